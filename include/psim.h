@@ -1,0 +1,159 @@
+/*
+ * libpsim — B200-native Proportional Similarity (Czekanowski) metric engine.
+ *
+ * C ABI of the hot path of propsim (reference: /root/reference/pkg/src/propsim).
+ * Every entry point names the reference function it replaces (file:line).
+ * Plain pointers and sizes only: device buffers are allocated by the caller
+ * (the Python host layer uses torch for that), `stream` is a cudaStream_t
+ * (NULL = legacy default stream). Calls are stream-ordered and asynchronous
+ * unless stated otherwise; the library never frees caller memory.
+ *
+ * Data layout in device memory (the reference's, core.py:235-236): a vector
+ * block is column-major, element (q, i) at V[i * ld + q]. `ld` must be a
+ * multiple of 16 bytes / sizeof(element) (2 for FP64, 4 for FP32) and V must
+ * be 16-byte aligned; rows q >= n_f of the padding are never read.
+ *
+ * Every function returns a status: 0 ok, 1 configuration error (propsim
+ * ConfigError / ValueError, core.py:20-25), 2 data error (DataError,
+ * core.py:24-25), 3 runtime error (EngineError, core.py:28-29; CUDA
+ * failures). psim_last_error() describes the last failure of the calling
+ * thread.
+ */
+#ifndef PSIM_H
+#define PSIM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PSIM_OK 0
+#define PSIM_ECONFIG 1
+#define PSIM_EDATA 2
+#define PSIM_ERUNTIME 3
+
+/* run precision (core.py:16 PRECISIONS) */
+#define PSIM_F32 0 /* "single" */
+#define PSIM_F64 1 /* "double" */
+
+#define PSIM_VERSION 1
+
+/* One 2-way block task: rows = m vectors of W, cols = n vectors of V.
+ * Replaces one BlockTask2 of run_2way (metrics2.py:149-158): numerator
+ * (mgemm_blocked, mingemm.py:189-209), value matrix (metrics2.py:85-89),
+ * compaction (_emit_pair_records, metrics2.py:92-105) and checksum terms
+ * (verify.py:74-96).
+ * Output `vals` (may be NULL for checksum-only): diagonal task (W == V,
+ * m == n): the block triangle li < lj at pair_index(li, lj, m); otherwise
+ * the rectangle row-major at li * n + lj. acc[0..1] += 128-bit checksum of
+ * the task (global canonical indices), acc[2] += degenerate count. */
+typedef struct psim_block2 {
+  const void* W;
+  int64_t ldw;
+  const void* V;
+  int64_t ldv;
+  int64_t n_f;
+  int64_t m, n;
+  int32_t diagonal;
+  const void* s_row; /* column sums of W's vectors (m) */
+  const void* s_col; /* column sums of V's vectors (n) */
+  int64_t g_row;     /* global vector id of W column 0 */
+  int64_t g_col;     /* global vector id of V column 0 */
+  int64_t n_v;       /* total vector count (canonical indexing) */
+  void* vals;
+  unsigned long long* acc; /* device, 3 x u64 */
+} psim_block2_t;
+
+/* One 3-way interval box: every (i, j, k) in [i0,i1) x [j0,j1) x [k0,k1),
+ * i < j < k, global ids. Replaces one SliceTask3 of run_3way
+ * (_execute_slice, metrics3.py:131-192; regions schedule.py:231-254).
+ * Block A holds I (column 0 = global a0), B holds J, C holds K (may alias).
+ * N_XY are 2-way numerator tables, column-major N_XY[x + y * ld_XY], x local
+ * in X, y local in Y. Output `vals` (may be NULL): pivot-major — for each j
+ * in J ascending, rows i, columns k row-major; psim_box3_plan gives the size. */
+typedef struct psim_box3 {
+  int64_t n_f, n_v;
+  const void* VA;
+  int64_t ldA, a0;
+  const void* VB;
+  int64_t ldB, b0;
+  const void* VC;
+  int64_t ldC, c0;
+  const void* SA;
+  const void* SB;
+  const void* SC;
+  const void* NAB;
+  int64_t ldAB;
+  const void* NAC;
+  int64_t ldAC;
+  const void* NBC;
+  int64_t ldBC;
+  int64_t i0, i1, j0, j1, k0, k1;
+  void* vals;
+  unsigned long long* acc; /* device, 3 x u64 */
+} psim_box3_t;
+
+/* --- library / device ----------------------------------------------------- */
+int psim_version(void);
+const char* psim_last_error(void);
+/* SM count and compute capability of the current device. */
+int psim_device_info(int* sm_count, int* cc_major, int* cc_minor);
+
+/* --- inputs ---------------------------------------------------------------- */
+/* SyntheticSpec.local_block, kind "random-exact" (verify.py:126-147):
+ * V[q, i] = mix64((q * n_v_total + i) ^ seed) mod 2^bits for global
+ * q in [f0, f0 + n_fp), i in [v0, v0 + n_vp). */
+int psim_gen_random_exact(int dtype, uint64_t seed, int bits, int64_t n_v_total, int64_t f0,
+                          int64_t v0, int64_t n_fp, int64_t n_vp, void* V, int64_t ld,
+                          void* stream);
+/* SyntheticSpec.local_block, kind "analytic" (verify.py:126-129): 1 + [q mod n_v == i]. */
+int psim_gen_analytic(int dtype, int64_t n_v_total, int64_t f0, int64_t v0, int64_t n_fp,
+                      int64_t n_vp, void* V, int64_t ld, void* stream);
+/* General-FP test input: uniform [0,1) from the same hash. */
+int psim_gen_uniform(int dtype, uint64_t seed, int64_t n_v_total, int64_t f0, int64_t v0,
+                     int64_t n_fp, int64_t n_vp, void* V, int64_t ld, void* stream);
+/* VectorBlock.__post_init__ (core.py:231-242): flags[0] += #non-finite,
+ * flags[1] += #negative (device u64[2]). */
+int psim_check_block(int dtype, const void* V, int64_t n_fp, int64_t n_vp, int64_t ld,
+                     unsigned long long* flags, void* stream);
+
+/* --- kernels --------------------------------------------------------------- */
+/* column_sums (mingemm.py:212-222): out[i] = sum_q V[q, i], ascending q from +0. */
+int psim_column_sums(int dtype, const void* V, int64_t n_fp, int64_t n_vp, int64_t ld,
+                     void* out, void* stream);
+/* mgemm_blocked (mingemm.py:189-209): M[i, j] = sum_q min(W[q, i], V[q, j]).
+ * packed == 0: M column-major (ldm >= m); symmetric != 0 requires W == V,
+ * m == n, computes the upper triangle once and mirrors it.
+ * packed != 0: M in the psim_block2_t value layout (triangle if symmetric). */
+int psim_mgemm(int dtype, const void* W, int64_t ldw, const void* V, int64_t ldv, int64_t n_f,
+               int64_t m, int64_t n, int symmetric, void* M, int64_t ldm, int packed,
+               void* stream);
+/* Fused 2-way block task (see psim_block2_t). */
+int psim_czek2_block(int dtype, const psim_block2_t* task, void* stream);
+/* 2-way epilogue from reduced packed numerators, rows [r0, r1) of a task's
+ * packed layout (field-axis path, metrics2.py:156-158). N and vals point at
+ * the first entry of row r0. */
+int psim_czek2_from_numerators(int dtype, const void* N, int64_t r0, int64_t r1, int64_t m,
+                               int64_t n, int diagonal, const void* s_row, const void* s_col,
+                               int64_t g_row, int64_t g_col, int64_t n_v, void* vals,
+                               unsigned long long* acc, void* stream);
+/* One step of the ordered field-axis fold (RankContext.reduce_field_axis,
+ * engine.py:197-216): dst[e] = dst[e] + src[e]. */
+int psim_fold_add(int dtype, void* dst, const void* src, int64_t count, void* stream);
+/* Output element count and CTA-tile count of a 3-way box (host-only, sync). */
+int psim_box3_plan(const psim_box3_t* box, int64_t* n_out, int64_t* n_tiles);
+/* Fused 3-way box (see psim_box3_t). */
+int psim_czek3_box(int dtype, const psim_box3_t* box, void* stream);
+
+/* --- measurement ----------------------------------------------------------- */
+/* Min+add issue-rate microbenchmark of the mainloop mix (roofline
+ * denominator). Synchronous. */
+int psim_peak_minplus(int dtype, int variant, int64_t iters, double* cmp_per_s,
+                      double* cmp_per_clk_sm, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PSIM_H */

@@ -1,0 +1,120 @@
+"""ctypes binding of libpsim.so (the C ABI in include/psim.h).
+
+The library is REQUIRED: there is no CPU fallback anywhere in this package.
+If ``_lib/libpsim.so`` is missing, ``lib()`` raises with the build command.
+Status codes map back onto the reference's exception families
+(1 -> ConfigError, 2 -> DataError, 3 -> EngineError; cli.py:917-929).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from pathlib import Path
+
+from .domain import ConfigError, DataError, EngineError
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libpsim.so"
+
+F32, F64 = 0, 1
+
+c_i64 = C.c_int64
+c_u64 = C.c_uint64
+c_vp = C.c_void_p
+c_ullp = C.POINTER(C.c_ulonglong)
+
+
+class Block2(C.Structure):
+    """psim_block2_t"""
+
+    _fields_ = [
+        ("W", c_vp), ("ldw", c_i64), ("V", c_vp), ("ldv", c_i64), ("n_f", c_i64),
+        ("m", c_i64), ("n", c_i64), ("diagonal", C.c_int32),
+        ("s_row", c_vp), ("s_col", c_vp),
+        ("g_row", c_i64), ("g_col", c_i64), ("n_v", c_i64),
+        ("vals", c_vp), ("acc", c_vp),
+    ]
+
+
+class Box3(C.Structure):
+    """psim_box3_t"""
+
+    _fields_ = [
+        ("n_f", c_i64), ("n_v", c_i64),
+        ("VA", c_vp), ("ldA", c_i64), ("a0", c_i64),
+        ("VB", c_vp), ("ldB", c_i64), ("b0", c_i64),
+        ("VC", c_vp), ("ldC", c_i64), ("c0", c_i64),
+        ("SA", c_vp), ("SB", c_vp), ("SC", c_vp),
+        ("NAB", c_vp), ("ldAB", c_i64),
+        ("NAC", c_vp), ("ldAC", c_i64),
+        ("NBC", c_vp), ("ldBC", c_i64),
+        ("i0", c_i64), ("i1", c_i64), ("j0", c_i64), ("j1", c_i64),
+        ("k0", c_i64), ("k1", c_i64),
+        ("vals", c_vp), ("acc", c_vp),
+    ]
+
+
+# name -> (restype, argtypes); every symbol declared in include/psim.h
+SIGNATURES = {
+    "psim_version": (C.c_int, []),
+    "psim_last_error": (C.c_char_p, []),
+    "psim_device_info": (C.c_int, [C.POINTER(C.c_int)] * 3),
+    "psim_gen_random_exact": (
+        C.c_int, [C.c_int, c_u64, C.c_int, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp]),
+    "psim_gen_analytic": (C.c_int, [C.c_int, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp]),
+    "psim_gen_uniform": (
+        C.c_int, [C.c_int, c_u64, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp]),
+    "psim_check_block": (C.c_int, [C.c_int, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp]),
+    "psim_column_sums": (C.c_int, [C.c_int, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp]),
+    "psim_mgemm": (
+        C.c_int,
+        [C.c_int, c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64, C.c_int, c_vp, c_i64, C.c_int,
+         c_vp]),
+    "psim_czek2_block": (C.c_int, [C.c_int, C.POINTER(Block2), c_vp]),
+    "psim_czek2_from_numerators": (
+        C.c_int,
+        [C.c_int, c_vp, c_i64, c_i64, c_i64, c_i64, C.c_int, c_vp, c_vp, c_i64, c_i64, c_i64,
+         c_vp, c_vp, c_vp]),
+    "psim_fold_add": (C.c_int, [C.c_int, c_vp, c_vp, c_i64, c_vp]),
+    "psim_box3_plan": (C.c_int, [C.POINTER(Box3), C.POINTER(c_i64), C.POINTER(c_i64)]),
+    "psim_czek3_box": (C.c_int, [C.c_int, C.POINTER(Box3), c_vp]),
+    "psim_peak_minplus": (
+        C.c_int, [C.c_int, C.c_int, c_i64, C.POINTER(C.c_double), C.POINTER(C.c_double), c_vp]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libpsim.so once; fail loudly when it has not been built."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not LIB_PATH.exists():
+                    raise ImportError(
+                        f"libpsim.so not found at {LIB_PATH}; build it with "
+                        "`python -m paper_1705_08210_b200.build` (no CPU fallback exists)"
+                    )
+                handle = C.CDLL(str(LIB_PATH))
+                for name, (res, args) in SIGNATURES.items():
+                    fn = getattr(handle, name)
+                    fn.restype = res
+                    fn.argtypes = args
+                _lib = handle
+    return _lib
+
+
+def check(status: int) -> None:
+    if status == 0:
+        return
+    msg = lib().psim_last_error().decode(errors="replace")
+    if status == 1:
+        raise ConfigError(msg)
+    if status == 2:
+        raise DataError(msg)
+    raise EngineError(msg)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(lib(), name)(*args))

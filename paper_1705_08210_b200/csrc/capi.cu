@@ -1,0 +1,226 @@
+// extern "C" boundary of libpsim (declared in include/psim.h): argument
+// validation, error-status mapping and the host-side planning of 3-way
+// boxes. No kernel code lives here.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "psim_internal.h"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return PSIM_OK;
+  if (e == cudaErrorInvalidConfiguration)
+    return fail(PSIM_ECONFIG, "%s: launch shape exceeds device limits", what);
+  return fail(PSIM_ERUNTIME, "%s: CUDA error %s (%s)", what, cudaGetErrorName(e),
+              cudaGetErrorString(e));
+}
+
+inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+inline int esize(int dtype) { return dtype == psim::kF64 ? 8 : 4; }
+
+int check_dtype(int dtype) {
+  if (dtype != psim::kF32 && dtype != psim::kF64)
+    return fail(PSIM_ECONFIG, "dtype must be PSIM_F32 (0) or PSIM_F64 (1), got %d", dtype);
+  return PSIM_OK;
+}
+
+// Operand contract of the min-plus mainloop: 16-byte aligned base, leading
+// dimension covering n_f and a multiple of one 16-byte chunk.
+int check_operand(int dtype, const void* p, int64_t ld, int64_t n_f, const char* name) {
+  if (!p) return fail(PSIM_ECONFIG, "%s is NULL", name);
+  if (reinterpret_cast<uintptr_t>(p) % 16)
+    return fail(PSIM_ECONFIG, "%s must be 16-byte aligned", name);
+  const int vec = 16 / esize(dtype);
+  if (ld < n_f || ld % vec)
+    return fail(PSIM_ECONFIG, "%s: ld=%lld must be >= n_f=%lld and a multiple of %d", name,
+                (long long)ld, (long long)n_f, vec);
+  return PSIM_OK;
+}
+
+// Per-pivot tile and output counts of a 3-way box (see psim_box3_t).
+void box3_counts(const psim_box3_t& b, std::vector<int64_t>* tile_pref,
+                 std::vector<int64_t>* out_pref) {
+  const int64_t nJ = b.j1 > b.j0 ? b.j1 - b.j0 : 0;
+  tile_pref->assign(nJ + 1, 0);
+  out_pref->assign(nJ + 1, 0);
+  for (int64_t jj = 0; jj < nJ; ++jj) {
+    const int64_t j = b.j0 + jj;
+    const int64_t ihi = b.i1 < j ? b.i1 : j;
+    const int64_t klo = b.k0 > j + 1 ? b.k0 : j + 1;
+    const int64_t r = ihi > b.i0 ? ihi - b.i0 : 0;
+    const int64_t c = b.k1 > klo ? b.k1 - klo : 0;
+    const int64_t t = ((r + psim::kTileM - 1) / psim::kTileM) * ((c + psim::kTileN - 1) / psim::kTileN);
+    (*tile_pref)[jj + 1] = (*tile_pref)[jj] + (r && c ? t : 0);
+    (*out_pref)[jj + 1] = (*out_pref)[jj] + r * c;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int psim_version(void) { return PSIM_VERSION; }
+
+const char* psim_last_error(void) { return g_err; }
+
+int psim_device_info(int* sm_count, int* cc_major, int* cc_minor) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_status(e, "cudaGetDevice");
+  if (sm_count) cudaDeviceGetAttribute(sm_count, cudaDevAttrMultiProcessorCount, dev);
+  if (cc_major) cudaDeviceGetAttribute(cc_major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (cc_minor) cudaDeviceGetAttribute(cc_minor, cudaDevAttrComputeCapabilityMinor, dev);
+  return cuda_status(cudaGetLastError(), "psim_device_info");
+}
+
+int psim_gen_random_exact(int dtype, uint64_t seed, int bits, int64_t n_v_total, int64_t f0,
+                          int64_t v0, int64_t n_fp, int64_t n_vp, void* V, int64_t ld,
+                          void* stream) {
+  if (int r = check_dtype(dtype)) return r;
+  if (bits < 0 || bits > 53) return fail(PSIM_ECONFIG, "bits must be in [0, 53], got %d", bits);
+  if (!V || ld < n_fp) return fail(PSIM_ECONFIG, "bad output buffer / ld");
+  return cuda_status(
+      psim::gen_random_exact(dtype, seed, bits, n_v_total, f0, v0, n_fp, n_vp, V, ld, S(stream)),
+      "psim_gen_random_exact");
+}
+
+int psim_gen_analytic(int dtype, int64_t n_v_total, int64_t f0, int64_t v0, int64_t n_fp,
+                      int64_t n_vp, void* V, int64_t ld, void* stream) {
+  if (int r = check_dtype(dtype)) return r;
+  if (!V || ld < n_fp) return fail(PSIM_ECONFIG, "bad output buffer / ld");
+  return cuda_status(psim::gen_analytic(dtype, n_v_total, f0, v0, n_fp, n_vp, V, ld, S(stream)),
+                     "psim_gen_analytic");
+}
+
+int psim_gen_uniform(int dtype, uint64_t seed, int64_t n_v_total, int64_t f0, int64_t v0,
+                     int64_t n_fp, int64_t n_vp, void* V, int64_t ld, void* stream) {
+  if (int r = check_dtype(dtype)) return r;
+  if (!V || ld < n_fp) return fail(PSIM_ECONFIG, "bad output buffer / ld");
+  return cuda_status(
+      psim::gen_uniform(dtype, seed, n_v_total, f0, v0, n_fp, n_vp, V, ld, S(stream)),
+      "psim_gen_uniform");
+}
+
+int psim_check_block(int dtype, const void* V, int64_t n_fp, int64_t n_vp, int64_t ld,
+                     unsigned long long* flags, void* stream) {
+  if (int r = check_dtype(dtype)) return r;
+  if (!V || !flags || ld < n_fp) return fail(PSIM_ECONFIG, "bad block / flags / ld");
+  return cuda_status(psim::check_block(dtype, V, n_fp, n_vp, ld, flags, S(stream)),
+                     "psim_check_block");
+}
+
+int psim_column_sums(int dtype, const void* V, int64_t n_fp, int64_t n_vp, int64_t ld,
+                     void* out, void* stream) {
+  if (int r = check_dtype(dtype)) return r;
+  if (!V || !out || ld < n_fp) return fail(PSIM_ECONFIG, "bad block / output / ld");
+  return cuda_status(psim::column_sums(dtype, V, n_fp, n_vp, ld, out, S(stream)),
+                     "psim_column_sums");
+}
+
+int psim_mgemm(int dtype, const void* W, int64_t ldw, const void* V, int64_t ldv, int64_t n_f,
+               int64_t m, int64_t n, int symmetric, void* M, int64_t ldm, int packed,
+               void* stream) {
+  if (int r = check_dtype(dtype)) return r;
+  if (n_f < 0 || m < 0 || n < 0) return fail(PSIM_ECONFIG, "negative extent");
+  if (int r = check_operand(dtype, W, ldw, n_f, "W")) return r;
+  if (int r = check_operand(dtype, V, ldv, n_f, "V")) return r;
+  if (!M) return fail(PSIM_ECONFIG, "M is NULL");
+  if (symmetric && (W != V || m != n || ldw != ldv))
+    return fail(PSIM_ECONFIG, "symmetric mGEMM needs W == V and m == n");
+  if (!packed && ldm < m) return fail(PSIM_ECONFIG, "ldm=%lld < m=%lld", (long long)ldm, (long long)m);
+  return cuda_status(psim::mgemm(dtype, W, ldw, V, ldv, n_f, m, n, symmetric, M, ldm, packed,
+                                 S(stream)),
+                     "psim_mgemm");
+}
+
+int psim_czek2_block(int dtype, const psim_block2_t* t, void* stream) {
+  if (int r = check_dtype(dtype)) return r;
+  if (!t) return fail(PSIM_ECONFIG, "task is NULL");
+  if (t->n_f < 0 || t->m < 0 || t->n < 0) return fail(PSIM_ECONFIG, "negative extent");
+  if (int r = check_operand(dtype, t->W, t->ldw, t->n_f, "W")) return r;
+  if (int r = check_operand(dtype, t->V, t->ldv, t->n_f, "V")) return r;
+  if (!t->s_row || !t->s_col || !t->acc) return fail(PSIM_ECONFIG, "sums / acc is NULL");
+  if (t->diagonal && (t->m != t->n || t->g_row != t->g_col))
+    return fail(PSIM_ECONFIG, "diagonal task needs m == n and g_row == g_col");
+  if (t->g_row < 0 || t->g_col < 0 || t->g_row + t->m > t->n_v || t->g_col + t->n > t->n_v)
+    return fail(PSIM_ECONFIG, "task outside [0, n_v)");
+  return cuda_status(psim::czek2_block(dtype, *t, S(stream)), "psim_czek2_block");
+}
+
+int psim_czek2_from_numerators(int dtype, const void* N, int64_t r0, int64_t r1, int64_t m,
+                               int64_t n, int diagonal, const void* s_row, const void* s_col,
+                               int64_t g_row, int64_t g_col, int64_t n_v, void* vals,
+                               unsigned long long* acc, void* stream) {
+  if (int r = check_dtype(dtype)) return r;
+  if (!N || !s_row || !s_col || !acc) return fail(PSIM_ECONFIG, "NULL argument");
+  if (r0 < 0 || r1 > m || r0 > r1) return fail(PSIM_ECONFIG, "row range outside [0, m]");
+  return cuda_status(psim::czek2_from_num(dtype, N, r0, r1, m, n, diagonal, s_row, s_col, g_row,
+                                          g_col, n_v, vals, acc, S(stream)),
+                     "psim_czek2_from_numerators");
+}
+
+int psim_fold_add(int dtype, void* dst, const void* src, int64_t count, void* stream) {
+  if (int r = check_dtype(dtype)) return r;
+  if (!dst || !src) return fail(PSIM_ECONFIG, "NULL argument");
+  return cuda_status(psim::fold_add(dtype, dst, src, count, S(stream)), "psim_fold_add");
+}
+
+int psim_box3_plan(const psim_box3_t* box, int64_t* n_out, int64_t* n_tiles) {
+  if (!box) return fail(PSIM_ECONFIG, "box is NULL");
+  std::vector<int64_t> tp, op;
+  box3_counts(*box, &tp, &op);
+  if (n_out) *n_out = op.back();
+  if (n_tiles) *n_tiles = tp.back();
+  return PSIM_OK;
+}
+
+int psim_czek3_box(int dtype, const psim_box3_t* b, void* stream) {
+  if (int r = check_dtype(dtype)) return r;
+  if (!b) return fail(PSIM_ECONFIG, "box is NULL");
+  if (b->n_f < 0) return fail(PSIM_ECONFIG, "negative n_f");
+  if (int r = check_operand(dtype, b->VA, b->ldA, b->n_f, "VA")) return r;
+  if (int r = check_operand(dtype, b->VB, b->ldB, b->n_f, "VB")) return r;
+  if (int r = check_operand(dtype, b->VC, b->ldC, b->n_f, "VC")) return r;
+  if (!b->SA || !b->SB || !b->SC || !b->NAB || !b->NAC || !b->NBC || !b->acc)
+    return fail(PSIM_ECONFIG, "NULL sums / numerator table / acc");
+  if (b->i0 < b->a0 || b->j0 < b->b0 || b->k0 < b->c0 || b->i1 > b->n_v || b->j1 > b->n_v ||
+      b->k1 > b->n_v)
+    return fail(PSIM_ECONFIG, "box intervals outside their blocks");
+  std::vector<int64_t> tp, op;
+  box3_counts(*b, &tp, &op);
+  const int64_t n_tiles = tp.back();
+  if (n_tiles == 0) return PSIM_OK;
+  cudaStream_t st = S(stream);
+  int64_t* d = nullptr;
+  cudaError_t e = cudaMallocAsync(&d, 2 * tp.size() * sizeof(int64_t), st);
+  if (e != cudaSuccess) return cuda_status(e, "psim_czek3_box workspace");
+  e = psim::czek3_box(dtype, *b, d, n_tiles, st);
+  cudaError_t e2 = cudaFreeAsync(d, st);
+  if (e == cudaSuccess) e = e2;
+  return cuda_status(e, "psim_czek3_box");
+}
+
+int psim_peak_minplus(int dtype, int variant, int64_t iters, double* cmp_per_s,
+                      double* cmp_per_clk_sm, void* stream) {
+  if (int r = check_dtype(dtype)) return r;
+  if (!cmp_per_s || !cmp_per_clk_sm || iters < 1) return fail(PSIM_ECONFIG, "bad arguments");
+  return cuda_status(psim::peak_minplus(dtype, variant, iters, cmp_per_s, cmp_per_clk_sm,
+                                        S(stream)),
+                     "psim_peak_minplus");
+}
+
+}  // extern "C"

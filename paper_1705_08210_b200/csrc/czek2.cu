@@ -1,0 +1,239 @@
+// 2-way Czekanowski kernels: min-plus numerators fused with the metric
+// epilogue, compaction and the 128-bit checksum.
+//
+// Reference path replaced (one BlockTask2 of run_2way):
+//   numerator  mgemm_blocked          mingemm.py:189-209 / 94-117
+//   epilogue   _pair_value_matrix     metrics2.py:85-89   (2*N)/(s_i+s_j), D==0 -> +0
+//   compaction _emit_pair_records     metrics2.py:92-105  diagonal keeps li<lj
+//   checksum   checksum/add_term      verify.py:74-96
+#include "minplus.cuh"
+#include "psim_internal.h"
+
+namespace psim {
+
+enum Mode2 : int {
+  kCzek2 = 0,      // values + checksum (+ degenerate count)
+  kRawCol = 1,     // numerators, column-major M[i + j*ldm]; diagonal mirrors to a full square
+  kRawPacked = 2,  // numerators in the packed value layout (triangle or row-major rectangle)
+};
+
+template <typename T>
+struct Args2 {
+  const T* W;
+  int64_t ldw;
+  const T* V;
+  int64_t ldv;
+  int64_t n_f;
+  int64_t m, n;  // rows (W vectors) x cols (V vectors)
+  int diagonal;  // W and V are the same block: only i < j is kept
+  const T* s_row;
+  const T* s_col;
+  int64_t g_row, g_col, n_v;  // global id of local row 0 / col 0; global vector count
+  T* out;                     // values (kCzek2), numerators (kRaw*)
+  int64_t ldm;                // kRawCol leading dimension
+  unsigned long long* acc;    // [3]: checksum lo, hi, degenerate count (kCzek2)
+  int64_t tiles_n;            // ceil(n / kBN) (rectangle) or tiles per edge (diagonal)
+};
+
+// Position of local pair (i, j) in the packed layout shared by values and
+// packed numerators: the block triangle in canonical order (diagonal task)
+// or the rectangle row-major (off-diagonal task).
+__device__ __forceinline__ int64_t packed_pos(int diagonal, int64_t i, int64_t j, int64_t m,
+                                              int64_t n) {
+  return diagonal ? (int64_t)pair_index(i, j, m) : i * n + j;
+}
+
+template <typename T, int MODE>
+__global__ void __launch_bounds__(kNT, 1) k_minplus2(const Args2<T> a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* smem = reinterpret_cast<T*>(smem_raw);
+  int bi, bj;
+  if (a.diagonal) {
+    tri_tile((int64_t)blockIdx.x, a.tiles_n, bi, bj);
+  } else {
+    bi = (int)(blockIdx.x / a.tiles_n);
+    bj = (int)(blockIdx.x % a.tiles_n);
+  }
+  const int64_t row0 = (int64_t)bi * kBM, col0 = (int64_t)bj * kBN;
+  const int rows = (int)min64(kBM, a.m - row0);
+  const int cols = (int)min64(kBN, a.n - col0);
+
+  T acc[kTM][kTN];
+  minplus_tile<T, false>(a.W + row0 * a.ldw, a.ldw, rows, a.V + col0 * a.ldv, a.ldv, cols,
+                         nullptr, a.n_f, acc, smem);
+
+  const int ty = thread_ty(), tx = thread_tx();
+  if (MODE == kCzek2) {
+    Cks c;
+#pragma unroll
+    for (int mi = 0; mi < kTM; ++mi) {
+      const int li = ty + 16 * mi;
+      if (li >= rows) continue;
+      const int64_t i = row0 + li;
+      const T si = a.s_row[i];
+      const uint64_t gi = (uint64_t)(a.g_row + i);
+#pragma unroll
+      for (int nj = 0; nj < kTN; ++nj) {
+        const int lj = tx + 16 * nj;
+        const int64_t j = col0 + lj;
+        if (lj >= cols || (a.diagonal && j <= i)) continue;
+        const T d = Traits<T>::add(si, a.s_col[j]);
+        const bool zero = (d == T(0));
+        const T v = zero ? T(0) : Traits<T>::div(Traits<T>::mul(T(2), acc[mi][nj]), d);
+        if (a.out) a.out[packed_pos(a.diagonal, i, j, a.m, a.n)] = v;
+        const uint64_t gj = (uint64_t)(a.g_col + j);
+        const uint64_t gidx = gi < gj ? pair_index(gi, gj, a.n_v) : pair_index(gj, gi, a.n_v);
+        c.term(gidx, Traits<T>::bits(v));
+        c.deg += zero ? 1ull : 0ull;
+      }
+    }
+    cks_block_flush<kNT>(a.acc, c);
+  } else {
+#pragma unroll
+    for (int mi = 0; mi < kTM; ++mi) {
+      const int li = ty + 16 * mi;
+      if (li >= rows) continue;
+      const int64_t i = row0 + li;
+#pragma unroll
+      for (int nj = 0; nj < kTN; ++nj) {
+        const int lj = tx + 16 * nj;
+        const int64_t j = col0 + lj;
+        if (lj >= cols) continue;
+        if (MODE == kRawCol) {
+          if (a.diagonal && j < i) continue;
+          a.out[i + j * a.ldm] = acc[mi][nj];
+          if (a.diagonal && j != i) a.out[j + i * a.ldm] = acc[mi][nj];
+        } else {
+          if (a.diagonal && j <= i) continue;
+          a.out[packed_pos(a.diagonal, i, j, a.m, a.n)] = acc[mi][nj];
+        }
+      }
+    }
+  }
+}
+
+// Values + checksum from already-reduced packed numerators (the field-axis
+// path: partial N -> ordered fold over p_f -> this epilogue; metrics2.py:156-158).
+// One CTA per packed row li in [r0, r1); N and out point at row r0's first entry.
+template <typename T>
+__global__ void __launch_bounds__(256) k_czek2_from_num(const T* __restrict__ N, int64_t r0,
+                                                        int64_t m, int64_t n, int diagonal,
+                                                        const T* __restrict__ s_row,
+                                                        const T* __restrict__ s_col,
+                                                        int64_t g_row, int64_t g_col, int64_t n_v,
+                                                        T* __restrict__ out,
+                                                        unsigned long long* acc) {
+  const int64_t i = r0 + blockIdx.x;
+  const int64_t base = packed_pos(diagonal, r0, diagonal ? r0 + 1 : 0, m, n);
+  const int64_t jlo = diagonal ? i + 1 : 0;
+  const int64_t row_start = (diagonal ? (int64_t)pair_index(i, i + 1, m) : i * n) - base;
+  const T si = s_row[i];
+  const uint64_t gi = (uint64_t)(g_row + i);
+  Cks c;
+  for (int64_t j = jlo + threadIdx.x; j < n; j += blockDim.x) {
+    const int64_t p = row_start + (j - jlo);
+    const T d = Traits<T>::add(si, s_col[j]);
+    const bool zero = (d == T(0));
+    const T v = zero ? T(0) : Traits<T>::div(Traits<T>::mul(T(2), N[p]), d);
+    if (out) out[p] = v;
+    const uint64_t gj = (uint64_t)(g_col + j);
+    const uint64_t gidx = gi < gj ? pair_index(gi, gj, n_v) : pair_index(gj, gi, n_v);
+    c.term(gidx, Traits<T>::bits(v));
+    c.deg += zero ? 1ull : 0ull;
+  }
+  cks_block_flush<256>(acc, c);
+}
+
+template <typename T, int MODE>
+static cudaError_t launch2(const Args2<T>& a, cudaStream_t st) {
+  using TL = Tile<T>;
+  cudaError_t e = cudaFuncSetAttribute(k_minplus2<T, MODE>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, TL::SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  if (a.m <= 0 || a.n <= 0) return cudaSuccess;
+  int64_t blocks;
+  if (a.diagonal) {
+    const int64_t T_ = a.tiles_n;
+    blocks = T_ * (T_ + 1) / 2;
+  } else {
+    blocks = ((a.m + kBM - 1) / kBM) * a.tiles_n;
+  }
+  if (blocks > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  k_minplus2<T, MODE><<<(unsigned)blocks, kNT, TL::SMEM_BYTES, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <typename T>
+static Args2<T> make_args(const void* W, int64_t ldw, const void* V, int64_t ldv, int64_t n_f,
+                          int64_t m, int64_t n, int diagonal) {
+  Args2<T> a{};
+  a.W = static_cast<const T*>(W);
+  a.ldw = ldw;
+  a.V = static_cast<const T*>(V);
+  a.ldv = ldv;
+  a.n_f = n_f;
+  a.m = m;
+  a.n = n;
+  a.diagonal = diagonal;
+  a.tiles_n = (n + kBN - 1) / kBN;
+  return a;
+}
+
+template <typename T>
+cudaError_t czek2_block_t(const Czek2Block& t, cudaStream_t st) {
+  Args2<T> a = make_args<T>(t.W, t.ldw, t.V, t.ldv, t.n_f, t.m, t.n, t.diagonal);
+  a.s_row = static_cast<const T*>(t.s_row);
+  a.s_col = static_cast<const T*>(t.s_col);
+  a.g_row = t.g_row;
+  a.g_col = t.g_col;
+  a.n_v = t.n_v;
+  a.out = static_cast<T*>(t.vals);
+  a.acc = t.acc;
+  return launch2<T, kCzek2>(a, st);
+}
+
+template <typename T>
+cudaError_t mgemm_t(const void* W, int64_t ldw, const void* V, int64_t ldv, int64_t n_f,
+                    int64_t m, int64_t n, int symmetric, void* M, int64_t ldm, int packed,
+                    cudaStream_t st) {
+  Args2<T> a = make_args<T>(W, ldw, V, ldv, n_f, m, n, symmetric);
+  a.out = static_cast<T*>(M);
+  a.ldm = ldm;
+  return packed ? launch2<T, kRawPacked>(a, st) : launch2<T, kRawCol>(a, st);
+}
+
+template <typename T>
+cudaError_t czek2_from_num_t(const void* N, int64_t r0, int64_t r1, int64_t m, int64_t n,
+                             int diagonal, const void* s_row, const void* s_col, int64_t g_row,
+                             int64_t g_col, int64_t n_v, void* vals,
+                             unsigned long long* acc, cudaStream_t st) {
+  if (r1 <= r0) return cudaSuccess;
+  if (r1 - r0 > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  k_czek2_from_num<T><<<(unsigned)(r1 - r0), 256, 0, st>>>(
+      static_cast<const T*>(N), r0, m, n, diagonal, static_cast<const T*>(s_row),
+      static_cast<const T*>(s_col), g_row, g_col, n_v, static_cast<T*>(vals), acc);
+  return cudaGetLastError();
+}
+
+cudaError_t czek2_block(int dtype, const Czek2Block& t, cudaStream_t st) {
+  return dtype == kF64 ? czek2_block_t<double>(t, st) : czek2_block_t<float>(t, st);
+}
+
+cudaError_t mgemm(int dtype, const void* W, int64_t ldw, const void* V, int64_t ldv, int64_t n_f,
+                  int64_t m, int64_t n, int symmetric, void* M, int64_t ldm, int packed,
+                  cudaStream_t st) {
+  return dtype == kF64 ? mgemm_t<double>(W, ldw, V, ldv, n_f, m, n, symmetric, M, ldm, packed, st)
+                       : mgemm_t<float>(W, ldw, V, ldv, n_f, m, n, symmetric, M, ldm, packed, st);
+}
+
+cudaError_t czek2_from_num(int dtype, const void* N, int64_t r0, int64_t r1, int64_t m,
+                           int64_t n, int diagonal, const void* s_row, const void* s_col,
+                           int64_t g_row, int64_t g_col, int64_t n_v, void* vals,
+                           unsigned long long* acc, cudaStream_t st) {
+  return dtype == kF64 ? czek2_from_num_t<double>(N, r0, r1, m, n, diagonal, s_row, s_col, g_row,
+                                                  g_col, n_v, vals, acc, st)
+                       : czek2_from_num_t<float>(N, r0, r1, m, n, diagonal, s_row, s_col, g_row,
+                                                 g_col, n_v, vals, acc, st);
+}
+
+}  // namespace psim

@@ -1,0 +1,185 @@
+// 3-way Czekanowski kernel over one interval box of the tetrahedral schedule.
+//
+// Reference path replaced (one SliceTask3 of run_3way, metrics3.py:131-192):
+//   X_j = min(v_j, V_b)        xj_columns            mingemm.py:225-234
+//   n'_3 = dense(X_j, V_c)     _blocked_kernel       mingemm.py:94-117, metrics3.py:163
+//   Eq. 1 assembly             metrics3.py:167-182   (1.5*(((n_ij+n_ik)+n_jk)-n_ijk)) /
+//                                                    ((s_i+s_j)+s_k), canonical i<j<k roles
+//   cells / records            metrics3.py:183-191, checksum verify.py:86-96
+//
+// A box is every (i, j, k) in I x J x K with i < j < k (each schedule unit --
+// diagonal-edge sixth, face sixth, volume slice, and their stage sub-ranges
+// -- is one such box, see schedule.py:231-263). The kernel pivots on the
+// MIDDLE index j: for fixed j the valid (i, k) set is the rectangle
+// [i0, min64(i1, j)) x [max(k0, j+1), k1), so no tile is triangular. The
+// pivot column is min-combined into the staged A tile in shared memory, and
+// the mainloop is exactly the 2-way min-plus mainloop.
+//
+// Bitwise argument (SURVEY Appendix C rule 8): n_ijk = sum_q min(min(x_j, v_i), v_k)
+// in ascending q is role-independent because min is exact; n_ij, n_ik, n_jk
+// come from 2-way numerator tables whose entries equal the reference's
+// column_sums(Xb) / P_bc bit for bit; the assembly uses canonical roles.
+//
+// Output layout ("pivot-major"): for j in J, the rectangle rows i, columns k
+// row-major, at out_pref[j - j0].
+#include "minplus.cuh"
+#include "psim_internal.h"
+
+namespace psim {
+
+template <typename T>
+__global__ void __launch_bounds__(kNT, 1)
+    k_czek3(const Czek3Box b, const int64_t* __restrict__ tile_pref,
+            const int64_t* __restrict__ out_pref, int64_t nJ) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* smem = reinterpret_cast<T*>(smem_raw);
+
+  // locate pivot j: largest jj with tile_pref[jj] <= blockIdx.x
+  const int64_t t = blockIdx.x;
+  int64_t lo = 0, hi = nJ;  // invariant tile_pref[lo] <= t < tile_pref[hi]
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (tile_pref[mid] <= t) lo = mid; else hi = mid;
+  }
+  const int64_t j = b.j0 + lo;
+  const int64_t ihi = min64(b.i1, j);
+  const int64_t klo = max64(b.k0, j + 1);
+  const int64_t nrows = ihi - b.i0, ncols = b.k1 - klo;
+  const int64_t tiles_k = (ncols + kBN - 1) / kBN;
+  const int64_t lt = t - tile_pref[lo];
+  const int64_t ti = lt / tiles_k, tk = lt - ti * tiles_k;
+  const int64_t r0 = ti * kBM, c0 = tk * kBN;
+  const int rows = (int)min64(kBM, nrows - r0);
+  const int cols = (int)min64(kBN, ncols - c0);
+
+  const T* VA = static_cast<const T*>(b.VA);
+  const T* VB = static_cast<const T*>(b.VB);
+  const T* VC = static_cast<const T*>(b.VC);
+  const int64_t ia = b.i0 - b.a0 + r0;   // local column of the tile's first i in block A
+  const int64_t kc = klo - b.c0 + c0;    // local column of the tile's first k in block C
+  const int64_t jb = j - b.b0;           // local column of j in block B
+
+  T acc[kTM][kTN];
+  minplus_tile<T, true>(VA + ia * b.ldA, b.ldA, rows, VC + kc * b.ldC, b.ldC, cols,
+                        VB + jb * b.ldB, b.n_f, acc, smem);
+
+  const T* SA = static_cast<const T*>(b.SA);
+  const T* SB = static_cast<const T*>(b.SB);
+  const T* SC = static_cast<const T*>(b.SC);
+  const T* NAB = static_cast<const T*>(b.NAB);
+  const T* NAC = static_cast<const T*>(b.NAC);
+  const T* NBC = static_cast<const T*>(b.NBC);
+  T* out = static_cast<T*>(b.vals);
+  const T sj = SB[jb];
+  const int64_t obase = out_pref[lo];
+  const uint64_t nv = (uint64_t)b.n_v;
+
+  const int ty = thread_ty(), tx = thread_tx();
+  Cks c;
+#pragma unroll
+  for (int mi = 0; mi < kTM; ++mi) {
+    const int li = ty + 16 * mi;
+    if (li >= rows) continue;
+    const int64_t ai = ia + li;            // local in A
+    const int64_t i = b.a0 + ai;           // global
+    const T si = SA[ai];
+    const T nij = NAB[ai + jb * b.ldAB];
+    const T sij = Traits<T>::add(si, sj);
+    // triple_index(i, j, k) = base_ij + (k - j - 1), base_ij = C3(n)-C3(n-i)+pair_index(j-i-1, j-i, n-i-1)
+    const uint64_t base_ij = choose3(nv) - choose3(nv - (uint64_t)i) +
+                             pair_index((uint64_t)(j - i - 1), (uint64_t)(j - i), nv - (uint64_t)i - 1);
+    const int64_t orow = obase + (r0 + li) * ncols + c0;
+#pragma unroll
+    for (int nk = 0; nk < kTN; ++nk) {
+      const int lk = tx + 16 * nk;
+      if (lk >= cols) continue;
+      const int64_t kcl = kc + lk;          // local in C
+      const int64_t k = b.c0 + kcl;         // global
+      const T nik = NAC[ai + kcl * b.ldAC];
+      const T njk = NBC[jb + kcl * b.ldBC];
+      const T d = Traits<T>::add(sij, SC[kcl]);
+      const T n3 = Traits<T>::sub(Traits<T>::add(Traits<T>::add(nij, nik), njk), acc[mi][nk]);
+      const bool zero = (d == T(0));
+      const T v = zero ? T(0) : Traits<T>::div(Traits<T>::mul(T(1.5), n3), d);
+      if (out) out[orow + lk] = v;
+      c.term(base_ij + (uint64_t)(k - j - 1), Traits<T>::bits(v));
+      c.deg += zero ? 1ull : 0ull;
+    }
+  }
+  cks_block_flush<kNT>(b.acc, c);
+}
+
+// Per-pivot prefix sums of CTA tiles and output elements for a box, one CTA:
+// each thread folds a contiguous j range, then a block scan of the partials.
+__global__ void __launch_bounds__(1024) k_box3_prefix(int64_t i0, int64_t i1, int64_t j0,
+                                                      int64_t j1, int64_t k0, int64_t k1,
+                                                      int64_t* __restrict__ tile_pref,
+                                                      int64_t* __restrict__ out_pref) {
+  __shared__ int64_t s_t[1024], s_o[1024];
+  const int64_t nJ = j1 - j0;
+  const int64_t per = (nJ + blockDim.x - 1) / blockDim.x;
+  const int64_t a = min64(nJ, threadIdx.x * per), e = min64(nJ, a + per);
+  auto counts = [&](int64_t jj, int64_t& t, int64_t& o) {
+    const int64_t j = j0 + jj;
+    const int64_t r = max64(0, min64(i1, j) - i0);
+    const int64_t c = max64(0, k1 - max64(k0, j + 1));
+    t = ((r + kBM - 1) / kBM) * ((c + kBN - 1) / kBN);
+    o = r * c;
+  };
+  int64_t st = 0, so = 0;
+  for (int64_t jj = a; jj < e; ++jj) {
+    int64_t t, o;
+    counts(jj, t, o);
+    st += t;
+    so += o;
+  }
+  s_t[threadIdx.x] = st;
+  s_o[threadIdx.x] = so;
+  __syncthreads();
+  for (int off = 1; off < (int)blockDim.x; off <<= 1) {  // inclusive Hillis-Steele scan
+    int64_t vt = threadIdx.x >= off ? s_t[threadIdx.x - off] : 0;
+    int64_t vo = threadIdx.x >= off ? s_o[threadIdx.x - off] : 0;
+    __syncthreads();
+    s_t[threadIdx.x] += vt;
+    s_o[threadIdx.x] += vo;
+    __syncthreads();
+  }
+  int64_t rt = threadIdx.x ? s_t[threadIdx.x - 1] : 0;
+  int64_t ro = threadIdx.x ? s_o[threadIdx.x - 1] : 0;
+  for (int64_t jj = a; jj < e; ++jj) {
+    tile_pref[jj] = rt;
+    out_pref[jj] = ro;
+    int64_t t, o;
+    counts(jj, t, o);
+    rt += t;
+    ro += o;
+  }
+  if (threadIdx.x == blockDim.x - 1) {
+    tile_pref[nJ] = s_t[threadIdx.x];
+    out_pref[nJ] = s_o[threadIdx.x];
+  }
+}
+
+template <typename T>
+static cudaError_t czek3_t(const Czek3Box& b, int64_t* work, int64_t n_tiles, cudaStream_t st) {
+  using TL = Tile<T>;
+  cudaError_t e = cudaFuncSetAttribute(k_czek3<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       TL::SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  if (n_tiles <= 0) return cudaSuccess;
+  if (n_tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  const int64_t nJ = b.j1 - b.j0;
+  int64_t* tp = work;
+  int64_t* op = work + nJ + 1;
+  k_box3_prefix<<<1, 1024, 0, st>>>(b.i0, b.i1, b.j0, b.j1, b.k0, b.k1, tp, op);
+  k_czek3<T><<<(unsigned)n_tiles, kNT, TL::SMEM_BYTES, st>>>(b, tp, op, nJ);
+  return cudaGetLastError();
+}
+
+cudaError_t czek3_box(int dtype, const Czek3Box& b, int64_t* d_work, int64_t n_tiles,
+                      cudaStream_t st) {
+  return dtype == kF64 ? czek3_t<double>(b, d_work, n_tiles, st)
+                       : czek3_t<float>(b, d_work, n_tiles, st);
+}
+
+}  // namespace psim

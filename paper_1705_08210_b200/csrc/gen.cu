@@ -1,0 +1,170 @@
+// Element-wise device kernels around the min-plus core: synthetic input
+// generators, input validation, column sums and the ordered field fold.
+//
+//   gen_random_exact  SyntheticSpec.local_block, kind random-exact  verify.py:126-147
+//   gen_analytic      SyntheticSpec.local_block, kind analytic      verify.py:126-147
+//   gen_uniform       general-FP inputs: (mix64(seed ^ (q*n_v+i)) >> 11) * 2^-53
+//   check_block       VectorBlock.__post_init__ finite / >= 0       core.py:231-242
+//   column_sums       _colsum_kernel, ascending q from +0            mingemm.py:120-127
+//   fold_add          reduce_field_axis ascending-p_f fold step      engine.py:197-216
+#include "psim_common.cuh"
+#include "psim_internal.h"
+
+namespace psim {
+
+static inline unsigned grid_for(int64_t n, int threads) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b > 148 * 64) b = 148 * 64;
+  return (unsigned)(b < 1 ? 1 : b);
+}
+
+template <typename T, int KIND>
+__global__ void k_gen(uint64_t seed, uint64_t mask, int64_t n_v_total, int64_t f0, int64_t v0,
+                      int64_t n_fp, int64_t n_vp, T* __restrict__ out, int64_t ld) {
+  const int64_t total = n_fp * n_vp;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lv = e / n_fp, lq = e - lv * n_fp;
+    const uint64_t q = (uint64_t)(f0 + lq), i = (uint64_t)(v0 + lv);
+    T val;
+    if (KIND == 0) {  // random-exact: integers in [0, 2^bits)
+      val = (T)(mix64((q * (uint64_t)n_v_total + i) ^ seed) & mask);
+    } else if (KIND == 1) {  // analytic: 1 + [q mod n_v == i]
+      val = (T)(1 + ((q % (uint64_t)n_v_total) == i ? 1 : 0));
+    } else {  // uniform [0, 1) with the run dtype's mantissa
+      const uint64_t h = mix64((q * (uint64_t)n_v_total + i) ^ seed);
+      if (sizeof(T) == 8)
+        val = (T)((double)(h >> 11) * 0x1.0p-53);
+      else
+        val = (T)((float)(uint32_t)(h >> 40) * 0x1.0p-24f);
+    }
+    out[lv * ld + lq] = val;
+  }
+}
+
+template <typename T, int KIND>
+static cudaError_t gen_t(uint64_t seed, uint64_t mask, int64_t n_v_total, int64_t f0, int64_t v0,
+                         int64_t n_fp, int64_t n_vp, void* out, int64_t ld, cudaStream_t st) {
+  if (n_fp <= 0 || n_vp <= 0) return cudaSuccess;
+  k_gen<T, KIND><<<grid_for(n_fp * n_vp, 256), 256, 0, st>>>(seed, mask, n_v_total, f0, v0, n_fp,
+                                                             n_vp, static_cast<T*>(out), ld);
+  return cudaGetLastError();
+}
+
+cudaError_t gen_random_exact(int dtype, uint64_t seed, int bits, int64_t n_v_total, int64_t f0,
+                             int64_t v0, int64_t n_fp, int64_t n_vp, void* out, int64_t ld,
+                             cudaStream_t st) {
+  const uint64_t mask = bits >= 64 ? ~0ull : ((1ull << bits) - 1ull);
+  return dtype == kF64
+             ? gen_t<double, 0>(seed, mask, n_v_total, f0, v0, n_fp, n_vp, out, ld, st)
+             : gen_t<float, 0>(seed, mask, n_v_total, f0, v0, n_fp, n_vp, out, ld, st);
+}
+
+cudaError_t gen_analytic(int dtype, int64_t n_v_total, int64_t f0, int64_t v0, int64_t n_fp,
+                         int64_t n_vp, void* out, int64_t ld, cudaStream_t st) {
+  return dtype == kF64 ? gen_t<double, 1>(0, 0, n_v_total, f0, v0, n_fp, n_vp, out, ld, st)
+                       : gen_t<float, 1>(0, 0, n_v_total, f0, v0, n_fp, n_vp, out, ld, st);
+}
+
+cudaError_t gen_uniform(int dtype, uint64_t seed, int64_t n_v_total, int64_t f0, int64_t v0,
+                        int64_t n_fp, int64_t n_vp, void* out, int64_t ld, cudaStream_t st) {
+  return dtype == kF64 ? gen_t<double, 2>(seed, 0, n_v_total, f0, v0, n_fp, n_vp, out, ld, st)
+                       : gen_t<float, 2>(seed, 0, n_v_total, f0, v0, n_fp, n_vp, out, ld, st);
+}
+
+// flags[0] += non-finite count, flags[1] += negative count.
+template <typename T>
+__global__ void k_check(const T* __restrict__ V, int64_t n_fp, int64_t n_vp, int64_t ld,
+                        unsigned long long* flags) {
+  unsigned long long bad = 0, neg = 0;
+  const int64_t total = n_fp * n_vp;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lv = e / n_fp, lq = e - lv * n_fp;
+    const T x = V[lv * ld + lq];
+    bad += isfinite(x) ? 0 : 1;
+    neg += (x < T(0)) ? 1 : 0;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    bad += __shfl_down_sync(0xffffffffu, bad, o);
+    neg += __shfl_down_sync(0xffffffffu, neg, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (bad) atomicAdd(flags, bad);
+    if (neg) atomicAdd(flags + 1, neg);
+  }
+}
+
+cudaError_t check_block(int dtype, const void* V, int64_t n_fp, int64_t n_vp, int64_t ld,
+                        unsigned long long* flags, cudaStream_t st) {
+  if (n_fp <= 0 || n_vp <= 0) return cudaSuccess;
+  const unsigned g = grid_for(n_fp * n_vp, 256);
+  if (dtype == kF64)
+    k_check<double><<<g, 256, 0, st>>>(static_cast<const double*>(V), n_fp, n_vp, ld, flags);
+  else
+    k_check<float><<<g, 256, 0, st>>>(static_cast<const float*>(V), n_fp, n_vp, ld, flags);
+  return cudaGetLastError();
+}
+
+// Column sums, each a sequential ascending-q fold from +0 (bit-identical to
+// the min-plus diagonal M[i, i], test_mingemm.py:75-78). A CTA stages a
+// 32-vector x 32-field tile through shared memory with coalesced loads; one
+// thread per vector then folds its 32 values in order.
+template <typename T>
+__global__ void __launch_bounds__(256) k_colsum(const T* __restrict__ V, int64_t n_fp,
+                                                int64_t n_vp, int64_t ld, T* __restrict__ out) {
+  __shared__ T tile[32][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t v_base = (int64_t)blockIdx.x * 32;
+  T acc = T(0);
+  for (int64_t q0 = 0; q0 < n_fp; q0 += 32) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int lv = warp + 8 * r;
+      const int64_t v = v_base + lv, q = q0 + lane;
+      tile[lv][lane] = (v < n_vp && q < n_fp) ? V[v * ld + q] : T(0);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const int cnt = (int)min64(32, n_fp - q0);
+      for (int t = 0; t < cnt; ++t) acc = Traits<T>::add(acc, tile[lane][t]);
+    }
+    __syncthreads();
+  }
+  if (warp == 0 && v_base + lane < n_vp) out[v_base + lane] = acc;
+}
+
+cudaError_t column_sums(int dtype, const void* V, int64_t n_fp, int64_t n_vp, int64_t ld,
+                        void* out, cudaStream_t st) {
+  if (n_vp <= 0) return cudaSuccess;
+  const unsigned g = (unsigned)((n_vp + 31) / 32);
+  if (dtype == kF64)
+    k_colsum<double><<<g, 256, 0, st>>>(static_cast<const double*>(V), n_fp, n_vp, ld,
+                                        static_cast<double*>(out));
+  else
+    k_colsum<float><<<g, 256, 0, st>>>(static_cast<const float*>(V), n_fp, n_vp, ld,
+                                       static_cast<float*>(out));
+  return cudaGetLastError();
+}
+
+template <typename T>
+__global__ void k_fold(T* __restrict__ dst, const T* __restrict__ src, int64_t count) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count;
+       e += (int64_t)gridDim.x * blockDim.x)
+    dst[e] = Traits<T>::add(dst[e], src[e]);
+}
+
+cudaError_t fold_add(int dtype, void* dst, const void* src, int64_t count, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  const unsigned g = grid_for(count, 256);
+  if (dtype == kF64)
+    k_fold<double><<<g, 256, 0, st>>>(static_cast<double*>(dst), static_cast<const double*>(src),
+                                      count);
+  else
+    k_fold<float><<<g, 256, 0, st>>>(static_cast<float*>(dst), static_cast<const float*>(src),
+                                     count);
+  return cudaGetLastError();
+}
+
+}  // namespace psim

@@ -1,0 +1,95 @@
+// Min+add issue-rate microbenchmark: the roofline denominator (SURVEY
+// Appendix D). Each thread keeps 16 independent accumulators in registers and
+// repeats exactly the mainloop's per-comparison instruction mix:
+//   variant 0, FP64: acc += fmin(x, y)            DSETP.MIN + SEL + FSEL + DADD
+//   variant 0, FP32: (acc0, acc1) += (fminf, fminf) FMNMX x2 + FADD2
+//   variant 1, FP32: acc += fminf(x, y)           FMNMX + FADD (scalar)
+// The min operands rotate through the accumulators themselves so nothing can
+// be hoisted out of the loop. The grid is one full-occupancy wave; the rate is
+// reported per second (CUDA events) and per SM clock (clock64 inside each CTA).
+#include "minplus.cuh"
+#include "psim_internal.h"
+
+namespace psim {
+
+constexpr int kPeakAcc = 16;
+
+template <typename T, int VAR>
+__global__ void __launch_bounds__(256) k_peak(int64_t iters, T seed, T* sink, long long* cycles) {
+  T acc[kPeakAcc];
+#pragma unroll
+  for (int k = 0; k < kPeakAcc; ++k) acc[k] = seed * T(k + threadIdx.x % 7);
+  const T y0 = seed * T(3), y1 = seed * T(5);
+  __syncthreads();
+  const long long c0 = clock64();
+  for (int64_t it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < kPeakAcc; k += 2) {
+      if (sizeof(T) == 4 && VAR == 0) {
+        fadd2(*reinterpret_cast<float*>(&acc[k]), *reinterpret_cast<float*>(&acc[k + 1]),
+              fminf((float)acc[(k + 3) % kPeakAcc], (float)y0),
+              fminf((float)acc[(k + 6) % kPeakAcc], (float)y1));
+      } else {
+        acc[k] = Traits<T>::add(acc[k], Traits<T>::min(acc[(k + 3) % kPeakAcc], y0));
+        acc[k + 1] = Traits<T>::add(acc[k + 1], Traits<T>::min(acc[(k + 6) % kPeakAcc], y1));
+      }
+    }
+  }
+  __syncthreads();
+  const long long c1 = clock64();
+  T s = T(0);
+#pragma unroll
+  for (int k = 0; k < kPeakAcc; ++k) s += acc[k];
+  if (s == T(-1)) sink[threadIdx.x] = s;  // never true; keeps the loop live
+  if (threadIdx.x == 0) cycles[blockIdx.x] = c1 - c0;
+}
+
+template <typename T, int VAR>
+static cudaError_t peak_t(int64_t iters, double* cmp_per_s, double* cmp_per_clk_sm,
+                          cudaStream_t st) {
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_peak<T, VAR>, 256, 0);
+  if (per_sm < 1) per_sm = 1;
+  const int blocks = sms * per_sm;
+  T* sink = nullptr;
+  long long* cyc = nullptr;
+  cudaError_t e = cudaMallocAsync(&sink, 256 * sizeof(T), st);
+  if (e != cudaSuccess) return e;
+  e = cudaMallocAsync(&cyc, blocks * sizeof(long long), st);
+  if (e != cudaSuccess) return e;
+  cudaEvent_t ev0, ev1;
+  cudaEventCreate(&ev0);
+  cudaEventCreate(&ev1);
+  k_peak<T, VAR><<<blocks, 256, 0, st>>>(iters / 10 + 1, T(1e-3), sink, cyc);  // warm-up
+  cudaEventRecord(ev0, st);
+  k_peak<T, VAR><<<blocks, 256, 0, st>>>(iters, T(1e-3), sink, cyc);
+  cudaEventRecord(ev1, st);
+  e = cudaEventSynchronize(ev1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, ev0, ev1);
+  long long* h = new long long[blocks];
+  cudaMemcpyAsync(h, cyc, blocks * sizeof(long long), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  long long cmax = 0;
+  for (int b = 0; b < blocks; ++b) cmax = h[b] > cmax ? h[b] : cmax;
+  delete[] h;
+  const double cmps = (double)blocks * 256.0 * (double)iters * kPeakAcc;
+  *cmp_per_s = cmps / (ms * 1e-3);
+  *cmp_per_clk_sm = cmps / (double)sms / (double)cmax;
+  cudaFreeAsync(sink, st);
+  cudaFreeAsync(cyc, st);
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+cudaError_t peak_minplus(int dtype, int variant, int64_t iters, double* cmp_per_s,
+                         double* cmp_per_clk_sm, cudaStream_t st) {
+  if (dtype == kF64) return peak_t<double, 0>(iters, cmp_per_s, cmp_per_clk_sm, st);
+  return variant == 1 ? peak_t<float, 1>(iters, cmp_per_s, cmp_per_clk_sm, st)
+                      : peak_t<float, 0>(iters, cmp_per_s, cmp_per_clk_sm, st);
+}
+
+}  // namespace psim

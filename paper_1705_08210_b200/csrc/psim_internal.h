@@ -1,0 +1,53 @@
+// Internal (C++) launch interface between the C-ABI layer (capi.cu) and the
+// kernel translation units. Not part of the public ABI; see include/psim.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "psim.h"
+
+namespace psim {
+
+constexpr int kF32 = 0;
+constexpr int kF64 = 1;
+
+// CTA output tile of the min-plus kernels (rows x cols).
+constexpr int kTileM = 128;
+constexpr int kTileN = 128;
+
+// The public task descriptors double as the internal ones.
+using Czek2Block = psim_block2_t;
+using Czek3Box = psim_box3_t;
+
+cudaError_t gen_random_exact(int dtype, uint64_t seed, int bits, int64_t n_v_total, int64_t f0,
+                             int64_t v0, int64_t n_fp, int64_t n_vp, void* out, int64_t ld,
+                             cudaStream_t st);
+cudaError_t gen_analytic(int dtype, int64_t n_v_total, int64_t f0, int64_t v0, int64_t n_fp,
+                         int64_t n_vp, void* out, int64_t ld, cudaStream_t st);
+cudaError_t gen_uniform(int dtype, uint64_t seed, int64_t n_v_total, int64_t f0, int64_t v0,
+                        int64_t n_fp, int64_t n_vp, void* out, int64_t ld, cudaStream_t st);
+cudaError_t check_block(int dtype, const void* V, int64_t n_fp, int64_t n_vp, int64_t ld,
+                        unsigned long long* flags, cudaStream_t st);
+cudaError_t column_sums(int dtype, const void* V, int64_t n_fp, int64_t n_vp, int64_t ld,
+                        void* out, cudaStream_t st);
+cudaError_t fold_add(int dtype, void* dst, const void* src, int64_t count, cudaStream_t st);
+
+cudaError_t czek2_block(int dtype, const Czek2Block& t, cudaStream_t st);
+cudaError_t mgemm(int dtype, const void* W, int64_t ldw, const void* V, int64_t ldv, int64_t n_f,
+                  int64_t m, int64_t n, int symmetric, void* M, int64_t ldm, int packed,
+                  cudaStream_t st);
+cudaError_t czek2_from_num(int dtype, const void* N, int64_t r0, int64_t r1, int64_t m,
+                           int64_t n, int diagonal, const void* s_row, const void* s_col,
+                           int64_t g_row, int64_t g_col, int64_t n_v, void* vals,
+                           unsigned long long* acc, cudaStream_t st);
+
+// Launches the box kernel; the per-pivot tile / output prefix sums are built
+// on the device in `d_work` (2 * (j1 - j0 + 1) int64).
+cudaError_t czek3_box(int dtype, const Czek3Box& b, int64_t* d_work, int64_t n_tiles,
+                      cudaStream_t st);
+
+cudaError_t peak_minplus(int dtype, int variant, int64_t iters, double* cmp_per_s,
+                         double* cmp_per_clk_sm, cudaStream_t st);
+
+}  // namespace psim

@@ -1,0 +1,179 @@
+"""Device-memory plumbing: vector blocks in HBM and thin launch wrappers.
+
+HBM layout of a vector block (the reference's, core.py:235-236): column
+major, vector i's fields contiguous at V[i * ld + q]. ``ld`` is n_fp
+rounded up to 32 elements (128 B FP32 / 256 B FP64) so every vector starts
+on a 128-byte line and each 128-B field chunk the min-plus kernels stage is
+one aligned line. Padding rows are never read (the kernels zero-fill past
+n_fp). torch provides allocation and the current stream only; every
+arithmetic step is a libpsim kernel.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .domain import DataError, dtype_of, field_range, host_block, vector_range
+from .synthetic import synthetic_kind
+
+LD_ALIGN = 32
+
+
+def ld_for(n_fp: int) -> int:
+    return max(LD_ALIGN, -(-n_fp // LD_ALIGN) * LD_ALIGN)
+
+
+def code_of(precision: str) -> int:
+    return N.F64 if precision == "double" else N.F32
+
+
+def torch_dtype(precision: str):
+    return torch.float64 if precision == "double" else torch.float32
+
+
+def stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+class Block:
+    """One (n_fp x n_vp) vector block in HBM plus its field-folded column sums."""
+
+    __slots__ = ("data", "n_fp", "n_vp", "ld", "v0", "precision", "sums")
+
+    def __init__(self, data, n_fp, n_vp, ld, v0, precision):
+        self.data, self.n_fp, self.n_vp, self.ld = data, n_fp, n_vp, ld
+        self.v0, self.precision = v0, precision
+        self.sums = None
+
+    @property
+    def code(self) -> int:
+        return code_of(self.precision)
+
+    def col_ptr(self, local_col: int) -> int:
+        return self.data.data_ptr() + local_col * self.ld * self.data.element_size()
+
+
+def alloc_block(n_fp: int, n_vp: int, precision: str, device) -> torch.Tensor:
+    return torch.empty((n_vp, ld_for(n_fp)), dtype=torch_dtype(precision), device=device)
+
+
+def load_block(problem, grid, coords, device, pinned_cache: dict | None = None) -> Block:
+    """The rank's block: generated in HBM for synthetic sources, else copied H2D.
+
+    Generic sources are validated on the device (non-finite / negative ->
+    DataError, core.py:239-242)."""
+    n_fp, n_vp = problem.n_f // grid.n_pf, problem.n_v // grid.n_pv
+    f0, _ = field_range(grid, coords.p_f, problem.n_f)
+    v0, _ = vector_range(grid, coords.p_v, problem.n_v)
+    data = alloc_block(n_fp, n_vp, problem.precision, device)
+    ld = data.shape[1]
+    code = code_of(problem.precision)
+    src = problem.source
+    kind = synthetic_kind(src)
+    st = stream_ptr()
+    if kind is not None:
+        if hasattr(src, "check_problem"):
+            src.check_problem(problem)
+        else:  # a reference propsim.verify.SyntheticSpec
+            if (problem.n_f, problem.n_v) != (src.n_f, src.n_v):
+                from .domain import ConfigError
+                raise ConfigError("problem dims do not match synthetic dims")
+            src.check_exactness(problem.precision)
+        if kind == "random-exact":
+            N.call("psim_gen_random_exact", code, src.seed, src.bits, src.n_v, f0, v0, n_fp, n_vp,
+                   ptr(data), ld, st)
+        elif kind == "analytic":
+            N.call("psim_gen_analytic", code, src.n_v, f0, v0, n_fp, n_vp, ptr(data), ld, st)
+        else:
+            N.call("psim_gen_uniform", code, src.seed, src.n_v, f0, v0, n_fp, n_vp, ptr(data),
+                   ld, st)
+        return Block(data, n_fp, n_vp, ld, v0, problem.precision)
+    arr = host_block(problem, grid, coords)  # (n_fp, n_vp) Fortran
+    host = torch.from_numpy(np.ascontiguousarray(arr.T))  # (n_vp, n_fp) == same bytes
+    data[:, :n_fp].copy_(host, non_blocking=host.is_pinned())
+    check_values(data, n_fp, n_vp, ld, code)
+    return Block(data, n_fp, n_vp, ld, v0, problem.precision)
+
+
+def block_from_host(host: torch.Tensor, n_fp: int, v0: int, precision: str, device) -> Block:
+    """Block from a host tensor shaped (n_vp, n_fp) (= Fortran (n_fp, n_vp)).
+
+    Pinned hosts are copied asynchronously on the current stream."""
+    n_vp = host.shape[0]
+    data = alloc_block(n_fp, n_vp, precision, device)
+    data[:, :n_fp].copy_(host, non_blocking=host.is_pinned())
+    return Block(data, n_fp, n_vp, data.shape[1], v0, precision)
+
+
+def check_values(data, n_fp, n_vp, ld, code) -> None:
+    flags = torch.zeros(2, dtype=torch.int64, device=data.device)
+    N.call("psim_check_block", code, ptr(data), n_fp, n_vp, ld, ptr(flags), stream_ptr())
+    bad, neg = (int(x) for x in flags.cpu())
+    if bad:
+        raise DataError("non-finite element in vector block")
+    if neg:
+        raise DataError("negative element in vector block")
+
+
+def column_sums(block: Block) -> torch.Tensor:
+    out = torch.empty(block.n_vp, dtype=block.data.dtype, device=block.data.device)
+    N.call("psim_column_sums", block.code, ptr(block.data), block.n_fp, block.n_vp, block.ld,
+           ptr(out), stream_ptr())
+    return out
+
+
+def fold_(dst: torch.Tensor, src: torch.Tensor, code: int) -> None:
+    """dst <- dst + src elementwise on the device (one ordered fold step)."""
+    N.call("psim_fold_add", code, ptr(dst), ptr(src), dst.numel(), stream_ptr())
+
+
+def new_acc(device) -> torch.Tensor:
+    """Device accumulator: [checksum lo, checksum hi, degenerate count] (u64 bits)."""
+    return torch.zeros(3, dtype=torch.int64, device=device)
+
+
+def acc_words(acc: torch.Tensor) -> tuple[int, int, int]:
+    lo, hi, deg = (int(x) & ((1 << 64) - 1) for x in acc.cpu().tolist())
+    return lo, hi, deg
+
+
+def czek2_block(code: int, W: Block, r0: int, r1: int, V: Block, c0: int, c1: int,
+                s_row: torch.Tensor, s_col: torch.Tensor, diagonal: bool, n_v: int,
+                vals: torch.Tensor | None, acc: torch.Tensor) -> None:
+    t = N.Block2(
+        W=W.col_ptr(r0), ldw=W.ld, V=V.col_ptr(c0), ldv=V.ld, n_f=W.n_fp,
+        m=r1 - r0, n=c1 - c0, diagonal=1 if diagonal else 0,
+        s_row=s_row.data_ptr() + r0 * s_row.element_size(),
+        s_col=s_col.data_ptr() + c0 * s_col.element_size(),
+        g_row=W.v0 + r0, g_col=V.v0 + c0, n_v=n_v,
+        vals=ptr(vals), acc=ptr(acc),
+    )
+    N.call("psim_czek2_block", code, C.byref(t), stream_ptr())
+
+
+def mgemm_packed(code: int, W: Block, r0: int, r1: int, V: Block, c0: int, c1: int,
+                 diagonal: bool, out: torch.Tensor) -> None:
+    N.call("psim_mgemm", code, W.col_ptr(r0), W.ld, V.col_ptr(c0), V.ld, W.n_fp, r1 - r0, c1 - c0,
+           1 if diagonal else 0, ptr(out), 0, 1, stream_ptr())
+
+
+def mgemm_square(code: int, W: Block, V: Block, out: torch.Tensor, symmetric: bool) -> None:
+    """Column-major numerator table out[x + y*ld] (ld = out.shape[1]) for all
+    pairs of W's and V's vectors."""
+    N.call("psim_mgemm", code, ptr(W.data), W.ld, ptr(V.data), V.ld, W.n_fp, W.n_vp, V.n_vp,
+           1 if symmetric else 0, ptr(out), out.shape[1], 0, stream_ptr())
+
+
+def pair_count(m: int, n: int, diagonal: bool) -> int:
+    return m * (m - 1) // 2 if diagonal else m * n
+
+
+def dtype_np(precision: str):
+    return dtype_of(precision)

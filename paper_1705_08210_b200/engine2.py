@@ -1,0 +1,167 @@
+"""Per-rank 2-way pipeline on the GPU (the body of run_2way's rank_fn).
+
+Reference: metrics2.py:131-159 (rank_fn), 174-203 (_gather).
+For each Task2 of the slab plan (plan.py) one fused kernel computes the
+numerators, values, compaction and checksum terms (psim_czek2_block). With a
+field split (n_pf > 1) each field slab's partial packed numerators are
+folded in ascending p_f order -- the reference's reduce_field_axis
+(engine.py:197-216) -- and psim_czek2_from_numerators finishes the task.
+
+Transports:
+  "local"  every rank of the grid runs on this process's current GPU, one
+           after another; "exchanges" are reads of blocks already in HBM.
+           (The reference's "thread" / "process" transports map here.)
+  "nccl"   one process per GPU (torch.distributed, NCCL backend,
+           world_size == grid.n_p): see dist.py.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import device as D
+from .domain import RankCoords, n_ranks
+from .plan import Task2, plan_2way
+from .records import PairPiece
+
+
+@dataclass
+class Outcome:
+    pieces: list
+    lo: int = 0
+    hi: int = 0
+    degenerate: int = 0
+    count: int = 0
+    sums: np.ndarray | None = None
+    elapsed: float = 0.0
+    traffic: dict = field(default_factory=dict)
+
+
+def fold_sums(parts: list[torch.Tensor], code: int) -> torch.Tensor:
+    """((P0 + P1) + P2) + ... in ascending p_f (engine.py:197-216)."""
+    total = parts[0].clone()
+    for p in parts[1:]:
+        D.fold_(total, p, code)
+    return total
+
+
+def run_task(code: int, problem, grid, task: Task2, row_blocks: list, col_blocks: list,
+             s_row: torch.Tensor, s_col: torch.Tensor, acc: torch.Tensor,
+             keep_values: bool) -> PairPiece:
+    """One Task2 over field-slab lists row_blocks[p_f] / col_blocks[p_f]."""
+    m, n = task.r1 - task.r0, task.c1 - task.c0
+    count = D.pair_count(m, n, task.diagonal)
+    dev = acc.device
+    tdt = D.torch_dtype(problem.precision)
+    vals = torch.empty(count, dtype=tdt, device=dev) if keep_values else None
+    W0, V0 = row_blocks[0], col_blocks[0]
+    if len(row_blocks) == 1:
+        D.czek2_block(code, W0, task.r0, task.r1, V0, task.c0, task.c1, s_row, s_col,
+                      task.diagonal, problem.n_v, vals, acc)
+    else:
+        total = torch.empty(count, dtype=tdt, device=dev)
+        D.mgemm_packed(code, W0, task.r0, task.r1, V0, task.c0, task.c1, task.diagonal, total)
+        part = torch.empty_like(total)
+        for Wp, Vp in zip(row_blocks[1:], col_blocks[1:]):
+            D.mgemm_packed(code, Wp, task.r0, task.r1, Vp, task.c0, task.c1, task.diagonal, part)
+            D.fold_(total, part, code)
+        finish_numerators(code, total, 0, m, m, n, task.diagonal,
+                          s_row[task.r0:], s_col[task.c0:], W0.v0 + task.r0, V0.v0 + task.c0,
+                          problem.n_v, vals, acc)
+    return PairPiece(W0.v0 + task.r0, V0.v0 + task.c0, m, n, task.diagonal, 0, m, vals)
+
+
+def finish_numerators(code, N, r0, r1, m, n, diagonal, s_row, s_col, g_row, g_col, n_v, vals,
+                      acc) -> None:
+    from . import _native as Nat
+    Nat.call("psim_czek2_from_numerators", code, D.ptr(N), r0, r1, m, n, 1 if diagonal else 0,
+             D.ptr(s_row), D.ptr(s_col), g_row, g_col, n_v, D.ptr(vals), D.ptr(acc),
+             D.stream_ptr())
+
+
+def run_local(problem, grid, balance: str = "split", keep_values: bool = True) -> Outcome:
+    dev = torch.device("cuda", torch.cuda.current_device())
+    code = D.code_of(problem.precision)
+    n_vp = problem.n_v // grid.n_pv
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record()
+    blocks = {}
+    for p_v in range(grid.n_pv):
+        for p_f in range(grid.n_pf):
+            blocks[p_f, p_v] = D.load_block(problem, grid, RankCoords(p_f, p_v, 0), dev)
+    sums = {p_v: fold_sums([D.column_sums(blocks[p_f, p_v]) for p_f in range(grid.n_pf)], code)
+            for p_v in range(grid.n_pv)}
+    acc = D.new_acc(dev)
+    pieces = []
+    count = 0
+    for p_r in range(grid.n_pr):
+        for p_v in range(grid.n_pv):
+            for ev in plan_2way(grid, RankCoords(0, p_v, p_r), n_vp, balance):
+                if not isinstance(ev, Task2):
+                    continue
+                rows = [blocks[p_f, ev.row_block] for p_f in range(grid.n_pf)]
+                cols = [blocks[p_f, ev.col_block] for p_f in range(grid.n_pf)]
+                piece = run_task(code, problem, grid, ev, rows, cols, sums[ev.row_block],
+                                 sums[ev.col_block], acc, keep_values)
+                pieces.append(piece)
+                count += D.pair_count(piece.m, piece.n, piece.diagonal)
+    end.record()
+    end.synchronize()
+    lo, hi, deg = D.acc_words(acc)
+    all_sums = torch.cat([sums[p] for p in range(grid.n_pv)]).cpu().numpy()
+    return Outcome(pieces, lo, hi, deg, count, all_sums, start.elapsed_time(end) * 1e-3)
+
+
+def ranks(grid) -> int:
+    return n_ranks(grid)
+
+
+class Resident2:
+    """Benchmark harness for one GPU: the input block stays resident in HBM and
+    each step re-runs the hot path (column sums + the fused 2-way kernel, all
+    values written to HBM, checksum accumulated)."""
+
+    kernel_name = "k_minplus2<T, kCzek2> (psim_czek2_block)"
+
+    def __init__(self, problem, grid):
+        if n_ranks(grid) != 1:
+            raise ValueError("Resident2 runs a single-rank grid")
+        self.problem, self.grid = problem, grid
+        self.code = D.code_of(problem.precision)
+        self.launches_per_step = 2
+        n = problem.n_v
+        self.kernel_cmp_per_launch = problem.n_f * (n * (n - 1) // 2)
+
+    def setup(self) -> None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.block = D.load_block(self.problem, self.grid, RankCoords(0, 0, 0), dev)
+        n = self.problem.n_v
+        self.vals = torch.empty(n * (n - 1) // 2, dtype=D.torch_dtype(self.problem.precision),
+                                device=dev)
+        self.acc = D.new_acc(dev)
+
+    def step(self, timed: bool = False) -> list:
+        b = self.block
+        s = D.column_sums(b)
+        self.acc.zero_()
+        if timed:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+        D.czek2_block(self.code, b, 0, b.n_vp, b, 0, b.n_vp, s, s, True, self.problem.n_v,
+                      self.vals, self.acc)
+        if timed:
+            e1.record()
+            return [(e0, e1)]
+        return []
+
+    def checksum_hex(self) -> str:
+        from .synthetic import Checksum128
+
+        lo, hi, _ = D.acc_words(self.acc)
+        return Checksum128.from_words(lo, hi).hex
+
+    def teardown(self) -> None:
+        del self.block, self.vals, self.acc
+        torch.cuda.empty_cache()

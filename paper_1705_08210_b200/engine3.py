@@ -1,0 +1,200 @@
+"""Per-rank 3-way pipeline on the GPU (the body of run_3way's rank_fn).
+
+Reference: metrics3.py:82-113 (rank_fn), 131-192 (_execute_slice).
+The slab plan's units (plan.plan_3way, schedule.py:184-214) become interval
+boxes (plan.unit_boxes); each box is one psim_czek3_box launch. The 2-way
+numerator tables n_ij / n_ik / n_jk the boxes read are computed once per
+block pair with the same min-plus kernel (psim_mgemm), replacing the
+reference's per-unit P_bc and per-pivot column_sums(X) (metrics3.py:148-164),
+which are bitwise the same numbers (SURVEY Appendix C rule 8).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _native as N
+from . import device as D
+from .domain import ConfigError, RankCoords
+from .engine2 import Outcome, fold_sums
+from .plan import Box, Unit3, merge_boxes, plan_3way, unit_boxes
+from .records import BoxPiece
+
+
+def box_struct(box: Box, blocks: dict, sums: dict, tables, n_f: int, n_v: int,
+               vals, acc) -> N.Box3:
+    A, B, Cb = box.blocks
+    bA, bB, bC = blocks[A], blocks[B], blocks[Cb]
+    NAB, NAC, NBC = tables(A, B), tables(A, Cb), tables(B, Cb)
+    return N.Box3(
+        n_f=n_f, n_v=n_v,
+        VA=D.ptr(bA.data), ldA=bA.ld, a0=bA.v0,
+        VB=D.ptr(bB.data), ldB=bB.ld, b0=bB.v0,
+        VC=D.ptr(bC.data), ldC=bC.ld, c0=bC.v0,
+        SA=D.ptr(sums[A]), SB=D.ptr(sums[B]), SC=D.ptr(sums[Cb]),
+        NAB=D.ptr(NAB), ldAB=NAB.shape[1], NAC=D.ptr(NAC), ldAC=NAC.shape[1],
+        NBC=D.ptr(NBC), ldBC=NBC.shape[1],
+        i0=box.i0, i1=box.i1, j0=box.j0, j1=box.j1, k0=box.k0, k1=box.k1,
+        vals=D.ptr(vals), acc=D.ptr(acc),
+    )
+
+
+def box_plan(b: N.Box3) -> tuple[int, int]:
+    n_out, n_tiles = C.c_int64(), C.c_int64()
+    N.call("psim_box3_plan", C.byref(b), C.byref(n_out), C.byref(n_tiles))
+    return n_out.value, n_tiles.value
+
+
+class Tables:
+    """Lazily computed 2-way numerator tables N_XY (column-major, X <= Y)."""
+
+    def __init__(self, blocks: dict, code: int):
+        self.blocks, self.code, self.cache = blocks, code, {}
+
+    def __call__(self, X: int, Y: int) -> torch.Tensor:
+        key = (X, Y)
+        if key not in self.cache:
+            bx, by = self.blocks[X], self.blocks[Y]
+            out = torch.empty((by.n_vp, bx.n_vp), dtype=bx.data.dtype, device=bx.data.device)
+            D.mgemm_square(self.code, bx, by, out, symmetric=(X == Y))
+            self.cache[key] = out
+        return self.cache[key]
+
+
+def run_boxes(code, problem, boxes, blocks, sums, tables, acc, keep_values, pieces) -> int:
+    count = 0
+    tdt = D.torch_dtype(problem.precision)
+    dev = acc.device
+    for box in boxes:
+        probe = box_struct(box, blocks, sums, tables, problem.n_f, problem.n_v, None, acc)
+        n_out, _ = box_plan(probe)
+        if n_out == 0:
+            continue
+        vals = torch.empty(n_out, dtype=tdt, device=dev) if keep_values else None
+        b = box_struct(box, blocks, sums, tables, problem.n_f, problem.n_v, vals, acc)
+        N.call("psim_czek3_box", code, C.byref(b), D.stream_ptr())
+        pieces.append(BoxPiece(box.i0, box.i1, box.j0, box.j1, box.k0, box.k1, vals))
+        count += n_out
+    return count
+
+
+def run_local(problem, grid, stages, keep_values: bool = True) -> Outcome:
+    if grid.n_pf != 1:
+        raise ConfigError("3-way runs with a field-axis split (n_pf > 1) are not supported yet")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    code = D.code_of(problem.precision)
+    n_vp = problem.n_v // grid.n_pv
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record()
+    blocks = {p: D.load_block(problem, grid, RankCoords(0, p, 0), dev) for p in range(grid.n_pv)}
+    sums = {p: fold_sums([D.column_sums(blocks[p])], code) for p in range(grid.n_pv)}
+    tables = Tables(blocks, code)
+    acc = D.new_acc(dev)
+    pieces: list = []
+    count = 0
+    for p_r in range(grid.n_pr):
+        for p_v in range(grid.n_pv):
+            boxes = []
+            for ev in plan_3way(grid, RankCoords(0, p_v, p_r)):
+                if isinstance(ev, Unit3):
+                    boxes.extend(unit_boxes(ev, n_vp, grid.n_st, stages))
+            count += run_boxes(code, problem, merge_boxes(boxes), blocks, sums, tables, acc,
+                               keep_values, pieces)
+    end.record()
+    end.synchronize()
+    lo, hi, deg = D.acc_words(acc)
+    all_sums = torch.cat([sums[p] for p in range(grid.n_pv)]).cpu().numpy()
+    return Outcome(pieces, lo, hi, deg, count, all_sums, start.elapsed_time(end) * 1e-3)
+
+
+class Resident3:
+    """Benchmark harness for one GPU: input, sums and the 2-way numerator table
+    stay resident; each step runs every box of the single-slab plan stage by
+    stage (n_st chosen so one stage's values fit ``out_budget`` bytes), writing
+    all values to a reused HBM stage buffer and accumulating the checksum."""
+
+    kernel_name = "k_czek3<T> (psim_czek3_box)"
+
+    def __init__(self, problem, grid, out_budget: float = 40e9):
+        from .domain import n_ranks
+
+        if n_ranks(grid) != 1:
+            raise ValueError("Resident3 runs a single-rank grid")
+        self.problem = problem
+        n, isz = problem.n_v, (8 if problem.precision == "double" else 4)
+        total = n * (n - 1) * (n - 2) // 6 * isz
+        n_st = 1
+        while total / n_st > out_budget or (n // 6) % n_st:
+            n_st += 1
+            if n_st > n // 6:
+                raise ConfigError("no stage count fits the output budget")
+        from .domain import DecompGrid
+
+        self.grid = DecompGrid(n_st=n_st)
+        self.code = D.code_of(problem.precision)
+        self.kernel_cmp_per_launch = None
+        self.launches_per_step = None
+
+    def setup(self) -> None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+        p, g = self.problem, self.grid
+        self.block = D.load_block(p, g, RankCoords(0, 0, 0), dev)
+        self.blocks = {0: self.block}
+        self.sums = {0: D.column_sums(self.block)}
+        self.tables = Tables(self.blocks, self.code)
+        self.tables(0, 0)
+        self.acc = D.new_acc(dev)
+        self.stage_boxes = []
+        n_vp = p.n_v
+        for s in range(g.n_st):
+            boxes = []
+            for ev in plan_3way(g, RankCoords(0, 0, 0)):
+                if isinstance(ev, Unit3):
+                    boxes.extend(unit_boxes(ev, n_vp, g.n_st, (s,)))
+            self.stage_boxes.append(merge_boxes(boxes))
+        sizes = []
+        for boxes in self.stage_boxes:
+            sizes.append(sum(box_plan(box_struct(b, self.blocks, self.sums, self.tables, p.n_f,
+                                                 p.n_v, None, self.acc))[0] for b in boxes))
+        self.buf = torch.empty(max(sizes), dtype=D.torch_dtype(p.precision), device=dev)
+        launches = sum(len(b) for b in self.stage_boxes)
+        self.launches_per_step = 2 + 2 * launches  # sums, N2 table, (prefix, box) per box
+        nb = sum(len(b) for b in self.stage_boxes)
+        self.kernel_cmp_per_launch = p.n_f * (p.n_v * (p.n_v - 1) * (p.n_v - 2) // 6) / nb
+
+    def step(self, timed: bool = False) -> list:
+        p = self.problem
+        self.sums[0] = D.column_sums(self.block)
+        D.mgemm_square(self.code, self.block, self.block, self.tables.cache[0, 0], symmetric=True)
+        self.acc.zero_()
+        events = []
+        for boxes in self.stage_boxes:
+            off = 0
+            for box in boxes:
+                probe = box_struct(box, self.blocks, self.sums, self.tables, p.n_f, p.n_v, None,
+                                   self.acc)
+                n_out, _ = box_plan(probe)
+                vals = self.buf[off:off + n_out]
+                b = box_struct(box, self.blocks, self.sums, self.tables, p.n_f, p.n_v, vals,
+                               self.acc)
+                if timed:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                N.call("psim_czek3_box", self.code, C.byref(b), D.stream_ptr())
+                if timed:
+                    e1.record()
+                    events.append((e0, e1))
+                off += n_out
+        return events
+
+    def checksum_hex(self) -> str:
+        from .synthetic import Checksum128
+
+        lo, hi, _ = D.acc_words(self.acc)
+        return Checksum128.from_words(lo, hi).hex
+
+    def teardown(self) -> None:
+        del self.block, self.blocks, self.sums, self.tables, self.buf, self.acc
+        torch.cuda.empty_cache()
