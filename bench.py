@@ -215,7 +215,10 @@ def run_ours(args) -> dict | None:
     if world > 1:
         from paper_1705_08210_b200 import dist as PD
 
-        runner = PD.Runner2(prob, grid) if arity == 2 else PD.Runner3(prob, grid)
+        if arity == 2:
+            runner = PD.Runner2(prob, grid)
+        else:
+            runner = engine3.Runner3Dist(prob, grid, range(grid.n_st), out_budget=40e9)
     else:
         runner = engine2.Resident2(prob, grid) if arity == 2 else engine3.Resident3(prob, grid)
     runner.setup()

@@ -122,7 +122,8 @@ def _result(problem, grid, transport, out, stages) -> RunResult:
     expected = unique_tuple_count(problem.n_v, problem.arity)
     if stages is None and out.count != expected:
         raise EngineError(f"schedule covered {out.count} tuples, expected {expected}")
-    recs = LazyRecords(problem.arity, problem.n_v, out.pieces, out.sums, out.count,
+    local = out.count if out.local_count is None else out.local_count
+    recs = LazyRecords(problem.arity, problem.n_v, out.pieces, out.sums, local,
                        dtype_of(problem.precision))
     return RunResult(
         arity=problem.arity, n_f=problem.n_f, n_v=problem.n_v, precision=problem.precision,

@@ -25,13 +25,18 @@ __global__ void __launch_bounds__(256) k_peak(int64_t iters, T seed, T* sink, lo
   for (int64_t it = 0; it < iters; ++it) {
 #pragma unroll
     for (int k = 0; k < kPeakAcc; k += 2) {
-      if (sizeof(T) == 4 && VAR == 0) {
+      // Both min operands are per-thread vector registers that change every
+      // iteration (other accumulators), as in the mainloop where they come
+      // from LDS; VAR 2 uses a CTA-uniform operand (an optimistic bound).
+      const T u0 = VAR == 2 ? y0 : acc[(k + 5) % kPeakAcc];
+      const T u1 = VAR == 2 ? y1 : acc[(k + 11) % kPeakAcc];
+      if (sizeof(T) == 4 && VAR != 1) {
         fadd2(*reinterpret_cast<float*>(&acc[k]), *reinterpret_cast<float*>(&acc[k + 1]),
-              fminf((float)acc[(k + 3) % kPeakAcc], (float)y0),
-              fminf((float)acc[(k + 6) % kPeakAcc], (float)y1));
+              fminf((float)acc[(k + 3) % kPeakAcc], (float)u0),
+              fminf((float)acc[(k + 6) % kPeakAcc], (float)u1));
       } else {
-        acc[k] = Traits<T>::add(acc[k], Traits<T>::min(acc[(k + 3) % kPeakAcc], y0));
-        acc[k + 1] = Traits<T>::add(acc[k + 1], Traits<T>::min(acc[(k + 6) % kPeakAcc], y1));
+        acc[k] = Traits<T>::add(acc[k], Traits<T>::min(acc[(k + 3) % kPeakAcc], u0));
+        acc[k + 1] = Traits<T>::add(acc[k + 1], Traits<T>::min(acc[(k + 6) % kPeakAcc], u1));
       }
     }
   }
@@ -87,9 +92,12 @@ static cudaError_t peak_t(int64_t iters, double* cmp_per_s, double* cmp_per_clk_
 
 cudaError_t peak_minplus(int dtype, int variant, int64_t iters, double* cmp_per_s,
                          double* cmp_per_clk_sm, cudaStream_t st) {
-  if (dtype == kF64) return peak_t<double, 0>(iters, cmp_per_s, cmp_per_clk_sm, st);
-  return variant == 1 ? peak_t<float, 1>(iters, cmp_per_s, cmp_per_clk_sm, st)
-                      : peak_t<float, 0>(iters, cmp_per_s, cmp_per_clk_sm, st);
+  if (dtype == kF64)
+    return variant == 2 ? peak_t<double, 2>(iters, cmp_per_s, cmp_per_clk_sm, st)
+                        : peak_t<double, 0>(iters, cmp_per_s, cmp_per_clk_sm, st);
+  if (variant == 1) return peak_t<float, 1>(iters, cmp_per_s, cmp_per_clk_sm, st);
+  if (variant == 2) return peak_t<float, 2>(iters, cmp_per_s, cmp_per_clk_sm, st);
+  return peak_t<float, 0>(iters, cmp_per_s, cmp_per_clk_sm, st);
 }
 
 }  // namespace psim

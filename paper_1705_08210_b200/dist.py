@@ -1,0 +1,340 @@
+"""Multi-GPU runtime: one process per GPU, torch.distributed over NCCL.
+
+Replaces the reference's in-session transports (engine.py:158-216, 230-384):
+
+* block circulation (RankContext.send/receive, metrics2.py:140-147 and
+  metrics3.py:93-109) -> grouped NCCL send/recv (``batch_isend_irecv``),
+  issued one step ahead so the exchange of step d+1 overlaps the min-plus
+  kernel of step d;
+* the ordered field-axis fold (reduce_field_axis, engine.py:197-216) ->
+  an NCCL all-to-all of row chunks inside each field group, then every
+  rank folds its chunk's partials in ascending p_f order on the device
+  (bitwise the reference's ((P0 + P1) + P2) + ...)
+  and finishes the metric epilogue for those rows, so the reduction is a
+  reduce-scatter, not a broadcast;
+* result gathering (_gather, metrics2.py:174-203) -> an all-gather of each
+  rank's 128-bit checksum words, degenerate and record counts.
+
+The device work per rank is exactly the local engine's (engine2/engine3).
+``transport="nccl"`` requires world_size == grid.n_p; rank r takes the
+reference's coordinates coords_of_rank(r) (field-fastest, core.py:83-97).
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import device as D
+from .domain import ConfigError, RankCoords, coords_of_rank, n_ranks, rank_of_coords
+from .engine2 import Outcome, finish_numerators
+from .plan import Exchange, Task2, plan_2way
+from .records import PairPiece
+
+
+def ensure_initialized(grid) -> tuple[int, int]:
+    """Initialise the default NCCL group from the torchrun environment if needed."""
+    if not dist.is_initialized():
+        if "RANK" not in os.environ:
+            raise ConfigError("transport='nccl' needs a torch.distributed launch (torchrun)")
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    world, rank = dist.get_world_size(), dist.get_rank()
+    if world != n_ranks(grid):
+        raise ConfigError(f"transport='nccl' needs world_size == grid.n_p "
+                          f"({world} != {n_ranks(grid)})")
+    return world, rank
+
+
+_GROUPS: dict = {}
+
+
+def field_group(grid, coords):
+    """Process group of the ranks sharing (p_v, p_r) (one slab's field axis)."""
+    if grid.n_pf == 1:
+        return None
+    key = (grid.n_pf, grid.n_pv, grid.n_pr)
+    if key not in _GROUPS:
+        groups = {}
+        for p_r in range(grid.n_pr):
+            for p_v in range(grid.n_pv):
+                ranks = [rank_of_coords(RankCoords(f, p_v, p_r), grid) for f in range(grid.n_pf)]
+                groups[p_v, p_r] = dist.new_group(ranks)  # every rank creates every group
+        _GROUPS[key] = groups
+    return _GROUPS[key][coords.p_v, coords.p_r]
+
+
+def row_chunks(m: int, n: int, diagonal: bool, parts: int) -> list[tuple[int, int]]:
+    """Split rows [0, m) of a packed task into `parts` contiguous ranges of
+    about equal element count (triangle rows hold m-1-i entries)."""
+    if diagonal:
+        w = np.maximum(m - 1 - np.arange(m, dtype=np.int64), 0)
+    else:
+        w = np.full(m, n, dtype=np.int64)
+    cum = np.concatenate([[0], np.cumsum(w)])
+    total = int(cum[-1])
+    bounds = [0]
+    for p in range(1, parts):
+        bounds.append(int(np.searchsorted(cum, total * p / parts, side="left")))
+    bounds.append(m)
+    bounds = [min(max(b, 0), m) for b in bounds]
+    for i in range(1, len(bounds)):
+        bounds[i] = max(bounds[i], bounds[i - 1])
+    return [(bounds[i], bounds[i + 1]) for i in range(parts)]
+
+
+def packed_offset(row: int, m: int, n: int, diagonal: bool) -> int:
+    return row * (2 * m - row - 1) // 2 if diagonal else row * n
+
+
+def piece_count(pc) -> int:
+    if isinstance(pc, PairPiece):
+        return (packed_offset(pc.r1, pc.m, pc.n, pc.diagonal)
+                - packed_offset(pc.r0, pc.m, pc.n, pc.diagonal))
+    from .plan import Box, box_count
+
+    return box_count(Box((0, 0, 0), pc.i0, pc.i1, pc.j0, pc.j1, pc.k0, pc.k1))
+
+
+def gather_totals(acc: torch.Tensor, count: int, world: int, dev) -> tuple[int, int, int, int]:
+    """All-gather every rank's (checksum lo, hi, degenerate, count); sum mod 2^128."""
+    mine = torch.tensor([*acc.tolist(), count], dtype=torch.int64, device=dev)
+    allv = torch.empty(world * 4, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(allv, mine)
+    allv = allv.view(world, 4)
+    M64 = (1 << 64) - 1
+    total = deg = cnt = 0
+    for lo, hi, d, c in allv.cpu().tolist():
+        total += ((hi & M64) << 64) | (lo & M64)
+        deg += d
+        cnt += c
+    total &= (1 << 128) - 1
+    return total & M64, total >> 64, deg, cnt
+
+
+def reduce_scatter_rows(part: torch.Tensor, m: int, n: int, diagonal: bool, p_f: int, n_pf: int,
+                        group, fold) -> tuple[torch.Tensor, int, int]:
+    """Ordered field-axis reduction of one task's packed partial numerators.
+
+    Rows are cut into n_pf chunks of ~equal size; field rank f receives
+    chunk f from every field rank (one NCCL all-to-all) and folds the
+    partials as ((P0 + P1) + P2) + ... with ``fold(dst, src)`` -- the
+    reference's ascending-p_f fold (engine.py:197-216), bit for bit.
+    Returns (folded chunk, r0, r1)."""
+    chunks = row_chunks(m, n, diagonal, n_pf)
+    sizes = [packed_offset(b, m, n, diagonal) - packed_offset(a, m, n, diagonal)
+             for a, b in chunks]
+    mine = sizes[p_f]
+    recv = torch.empty(mine * n_pf, dtype=part.dtype, device=part.device)
+    dist.all_to_all_single(recv, part, output_split_sizes=[mine] * n_pf,
+                           input_split_sizes=sizes, group=group)
+    total = recv[:mine].clone()
+    for f in range(1, n_pf):
+        fold(total, recv[f * mine:(f + 1) * mine])
+    r0, r1 = chunks[p_f]
+    return total, r0, r1
+
+
+def fold_over_field(local_parts: torch.Tensor, code: int, group, n_pf: int) -> torch.Tensor:
+    """All-gather a small vector over the field group and fold in p_f order."""
+    out = torch.empty(n_pf * local_parts.numel(), dtype=local_parts.dtype,
+                      device=local_parts.device)
+    dist.all_gather_into_tensor(out, local_parts.contiguous(), group=group)
+    out = out.view((n_pf,) + tuple(local_parts.shape))
+    total = out[0].clone()
+    for p in range(1, n_pf):
+        D.fold_(total, out[p], code)
+    return total
+
+
+class Runner2:
+    """One rank's 2-way pipeline over NCCL (also the multi-GPU bench harness)."""
+
+    kernel_name = "k_minplus2<T, kCzek2> (psim_czek2_block)"
+
+    def __init__(self, problem, grid, balance: str = "split", keep_values: bool = True):
+        self.world, self.rank = ensure_initialized(grid)
+        self.problem, self.grid, self.balance, self.keep = problem, grid, balance, keep_values
+        self.coords = coords_of_rank(self.rank, grid)
+        self.code = D.code_of(problem.precision)
+        self.n_vp = problem.n_v // grid.n_pv
+        self.events = plan_2way(grid, self.coords, self.n_vp, balance)
+        self.group = field_group(grid, self.coords)
+        tasks = [e for e in self.events if isinstance(e, Task2)]
+        self.my_cmp = sum(problem.n_f // grid.n_pf * D.pair_count(t.r1 - t.r0, t.c1 - t.c0,
+                                                                   t.diagonal) for t in tasks)
+        self.kernel_cmp_per_launch = self.my_cmp / max(1, len(tasks))
+        self.launches_per_step = 1 + len(tasks) * (1 if grid.n_pf == 1 else 2 + grid.n_pf)
+
+    def peer(self, slab: int) -> int:
+        c = self.coords
+        return rank_of_coords(RankCoords(c.p_f, slab, c.p_r), self.grid)
+
+    def setup(self) -> None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.dev = dev
+        self.own = D.load_block(self.problem, self.grid, self.coords, dev)
+        self.remote = [D.Block(torch.empty_like(self.own.data), self.own.n_fp, self.own.n_vp,
+                               self.own.ld, 0, self.problem.precision) for _ in range(2)]
+        self.remote_sums = [torch.empty(self.n_vp, dtype=self.own.data.dtype, device=dev)
+                            for _ in range(2)]
+        self.acc = D.new_acc(dev)
+
+    def _sums(self) -> torch.Tensor:
+        s = D.column_sums(self.own)
+        if self.grid.n_pf > 1:
+            s = fold_over_field(s, self.code, self.group, self.grid.n_pf)
+        return s
+
+    def _post_exchange(self, ev: Exchange, slot: int, s_own: torch.Tensor):
+        ops = [
+            dist.P2POp(dist.isend, self.own.data, self.peer(ev.send_to)),
+            dist.P2POp(dist.isend, s_own, self.peer(ev.send_to)),
+            dist.P2POp(dist.irecv, self.remote[slot].data, self.peer(ev.recv_from)),
+            dist.P2POp(dist.irecv, self.remote_sums[slot], self.peer(ev.recv_from)),
+        ]
+        return dist.batch_isend_irecv(ops)
+
+    def step(self, timed: bool = False) -> list:
+        """Run this rank's whole plan once; returns (start, end) kernel events."""
+        p, g = self.problem, self.grid
+        self.acc.zero_()
+        s_own = self._sums()
+        pieces, events = [], []
+        evs = list(self.events)
+        exchanges = [e for e in evs if isinstance(e, Exchange)]
+        pending = {}
+        slot_of = {}
+        # post the first exchange before any compute; later ones one step ahead
+        if exchanges:
+            slot_of[exchanges[0].step] = 0
+            pending[exchanges[0].step] = self._post_exchange(exchanges[0], 0, s_own)
+        nxt = 1
+        for ev in evs:
+            if isinstance(ev, Exchange):
+                for w in pending.pop(ev.step):
+                    w.wait()
+                if nxt < len(exchanges):
+                    e2 = exchanges[nxt]
+                    slot_of[e2.step] = nxt % 2
+                    pending[e2.step] = self._post_exchange(e2, nxt % 2, s_own)
+                    nxt += 1
+                continue
+            if ev.diagonal:
+                V, s_col = self.own, s_own
+            else:
+                slot = slot_of[ev.step]
+                V, s_col = self.remote[slot], self.remote_sums[slot]
+                V.v0 = ev.col_block * self.n_vp
+            self.own.v0 = ev.row_block * self.n_vp
+            if timed:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+            pieces.extend(self._task(ev, V, s_own, s_col))
+            if timed:
+                e1.record()
+                events.append((e0, e1))
+        self.pieces = pieces
+        self.s_own = s_own
+        return events
+
+    def _task(self, t: Task2, V, s_row, s_col) -> list:
+        p, g = self.problem, self.grid
+        m, n = t.r1 - t.r0, t.c1 - t.c0
+        count = D.pair_count(m, n, t.diagonal)
+        tdt = D.torch_dtype(p.precision)
+        W = self.own
+        if g.n_pf == 1:
+            vals = torch.empty(count, dtype=tdt, device=self.dev) if self.keep else None
+            D.czek2_block(self.code, W, t.r0, t.r1, V, t.c0, t.c1, s_row, s_col, t.diagonal,
+                          p.n_v, vals, self.acc)
+            return [PairPiece(W.v0 + t.r0, V.v0 + t.c0, m, n, t.diagonal, 0, m, vals)]
+        # field split: partial packed numerators -> all-to-all row chunks -> ordered fold
+        part = torch.empty(count, dtype=tdt, device=self.dev)
+        D.mgemm_packed(self.code, W, t.r0, t.r1, V, t.c0, t.c1, t.diagonal, part)
+        total, r0, r1 = reduce_scatter_rows(part, m, n, t.diagonal, self.coords.p_f, g.n_pf,
+                                            self.group,
+                                            lambda dst, src: D.fold_(dst, src, self.code))
+        vals = torch.empty(total.numel(), dtype=tdt, device=self.dev) if self.keep else None
+        if r1 > r0:
+            finish_numerators(self.code, total, r0, r1, m, n, t.diagonal, s_row[t.r0:],
+                              s_col[t.c0:], W.v0 + t.r0, V.v0 + t.c0, p.n_v, vals, self.acc)
+        return [PairPiece(W.v0 + t.r0, V.v0 + t.c0, m, n, t.diagonal, r0, r1, vals)]
+
+    def checksum_hex(self) -> str:
+        lo, hi, _, _ = self.totals()
+        from .synthetic import Checksum128
+
+        return Checksum128.from_words(lo, hi).hex
+
+    def totals(self) -> tuple[int, int, int, int]:
+        """Global (lo, hi, degenerate, count) over all ranks."""
+        count = sum(piece_count(pc) for pc in self.pieces)
+        return gather_totals(self.acc, count, self.world, self.dev)
+
+    def global_sums(self) -> np.ndarray:
+        out = torch.empty(self.world * self.n_vp, dtype=self.s_own.dtype, device=self.dev)
+        dist.all_gather_into_tensor(out, self.s_own.contiguous())
+        out = out.view(self.world, self.n_vp)
+        host = out.cpu().numpy()
+        sums = np.empty(self.problem.n_v, dtype=host.dtype)
+        for r in range(self.world):
+            c = coords_of_rank(r, self.grid)
+            sums[c.p_v * self.n_vp:(c.p_v + 1) * self.n_vp] = host[r]
+        return sums
+
+    def teardown(self) -> None:
+        for name in ("own", "remote", "remote_sums", "acc", "pieces"):
+            if hasattr(self, name):
+                delattr(self, name)
+        torch.cuda.empty_cache()
+
+
+def run_2way_nccl(problem, grid, balance: str = "split", keep_values: bool = True) -> Outcome:
+    r = Runner2(problem, grid, balance, keep_values)
+    r.setup()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record()
+    r.step()
+    end.record()
+    end.synchronize()
+    el = torch.tensor([start.elapsed_time(end) * 1e-3], dtype=torch.float64, device=r.dev)
+    dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    lo, hi, deg, cnt = r.totals()
+    sums = r.global_sums()
+    pieces = r.pieces
+    return Outcome(pieces, lo, hi, deg, cnt, sums, float(el.item()),
+                   local_count=sum(piece_count(pc) for pc in pieces))
+
+
+def run_3way_nccl(problem, grid, stages, keep_values: bool = True) -> Outcome:
+    from .engine3 import Runner3Dist
+
+    r = Runner3Dist(problem, grid, stages, keep_values)
+    r.setup()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record()
+    r.step()
+    end.record()
+    end.synchronize()
+    el = torch.tensor([start.elapsed_time(end) * 1e-3], dtype=torch.float64, device=r.dev)
+    dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    lo, hi, deg, cnt = r.totals()
+    return Outcome(r.pieces, lo, hi, deg, cnt, r.global_sums(), float(el.item()),
+                   local_count=r.count)
+
+
+Runner3 = None  # set below (avoids an import cycle)
+
+
+def _bind():
+    global Runner3
+    from .engine3 import Runner3Dist
+
+    Runner3 = Runner3Dist
+
+
+_bind()

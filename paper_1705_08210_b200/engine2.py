@@ -37,6 +37,7 @@ class Outcome:
     sums: np.ndarray | None = None
     elapsed: float = 0.0
     traffic: dict = field(default_factory=dict)
+    local_count: int | None = None  # records held by this process (nccl: its share)
 
 
 def fold_sums(parts: list[torch.Tensor], code: int) -> torch.Tensor:

@@ -82,6 +82,17 @@ def _to_numpy(t) -> np.ndarray:
     return np.asarray(t)
 
 
+def _total(arity: int, n_v: int) -> int:
+    import math
+
+    return math.comb(n_v, arity)
+
+
+def _is_canonical_whole(piece, n_v: int) -> bool:
+    return (isinstance(piece, PairPiece) and piece.diagonal and piece.g_row == 0
+            and piece.m == n_v and piece.r0 == 0 and piece.r1 == piece.m)
+
+
 class LazyRecords(Sequence):
     """Sequence[MetricRecord] in canonical order, materialised on first use."""
 
@@ -106,15 +117,28 @@ class LazyRecords(Sequence):
             self._index = np.zeros(0, np.int64)
             self._values = np.zeros(0, self._dtype)
             return
-        idx = np.concatenate([p.canonical(self._n_v) for p in self._pieces])
-        val = np.concatenate([_to_numpy(p.values).reshape(-1) for p in self._pieces])
-        order = np.argsort(idx, kind="stable")
-        self._index, self._values = idx[order], val[order]
+        total = _total(self._arity, self._n_v)
+        if len(self._pieces) == 1 and _is_canonical_whole(self._pieces[0], self._n_v):
+            # one diagonal task over all vectors: already in canonical order
+            self._values = _to_numpy(self._pieces[0].values).reshape(-1)
+            self._index = None
+        else:
+            idx = np.concatenate([p.canonical(self._n_v) for p in self._pieces])
+            val = np.concatenate([_to_numpy(p.values).reshape(-1) for p in self._pieces])
+            if self._count == total:  # complete coverage: O(n) scatter, no sort
+                self._values = np.empty(total, dtype=val.dtype)
+                self._values[idx] = val
+                self._index = None
+            else:
+                order = np.argsort(idx, kind="stable")
+                self._index, self._values = idx[order], val[order]
         self._pieces = []  # release device memory references
 
     @property
     def canonical_indices(self) -> np.ndarray:
         self._build()
+        if self._index is None:
+            return np.arange(self._count, dtype=np.int64)
         return self._index
 
     @property
@@ -134,7 +158,7 @@ class LazyRecords(Sequence):
         return all(self._sums[i] == 0 for i in ids)
 
     def _record(self, pos: int) -> MetricRecord:
-        ids = self._tuple(int(self._index[pos]))
+        ids = self._tuple(pos if self._index is None else int(self._index[pos]))
         return MetricRecord(TupleId(ids), self._values[pos], self._degenerate(ids))
 
     def __getitem__(self, pos):

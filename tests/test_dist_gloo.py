@@ -1,0 +1,81 @@
+"""Multi-rank host logic on CPU (world_size 2, gloo): the ordered field-axis
+reduce-scatter and the global checksum gather of dist.py. The device folds
+are replaced by the same in-order elementwise add on CPU tensors."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1705_08210_b200 import dist as PD
+
+        out = {}
+        rng = np.random.default_rng(0)
+        for m, n, diagonal in ((37, 37, True), (11, 23, False), (2, 2, True)):
+            count = m * (m - 1) // 2 if diagonal else m * n
+            parts = [rng.random(count).astype(np.float32) for _ in range(world)]
+            mine = torch.from_numpy(parts[rank].copy())
+            total, r0, r1 = PD.reduce_scatter_rows(
+                mine, m, n, diagonal, rank, world, None, lambda d, s: d.add_(s))
+            a = PD.packed_offset(r0, m, n, diagonal)
+            b = PD.packed_offset(r1, m, n, diagonal)
+            want = parts[0][a:b].copy()
+            for p in parts[1:]:
+                want = want + p[a:b]  # ascending p_f fold
+            out[(m, n, diagonal)] = (bool((total.numpy() == want).all()), r0, r1)
+        # int64 words carry u64 bits (as the device accumulator does); the two
+        # low words sum past 2^64 so the carry into the high word is exercised
+        lo = -((1 << 63) - rank) if rank else -(1 << 63)
+        acc = torch.tensor([lo, rank, 2 + rank], dtype=torch.int64)
+        lo, hi, deg, cnt = PD.gather_totals(acc, 10 + rank, world, "cpu")
+        out["totals"] = (lo, hi, deg, cnt)
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_field_reduce_scatter_and_totals_gloo():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=180)
+        assert p.exitcode == 0
+    results = dict(q.get(timeout=10) for _ in range(world))
+    for key in ((37, 37, True), (11, 23, False), (2, 2, True)):
+        spans = []
+        for r in range(world):
+            ok, r0, r1 = results[r][key]
+            assert ok, (key, r)
+            spans.append((r0, r1))
+        m = key[0]
+        assert spans[0][0] == 0 and spans[-1][1] == m
+        assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+    # both ranks see the same global totals; lo words wrap with carry into hi
+    t0, t1 = results[0]["totals"], results[1]["totals"]
+    assert t0 == t1
+    M64 = (1 << 64) - 1
+    lo0 = (-(1 << 63)) & M64
+    lo1 = (-((1 << 63) - 1)) & M64
+    total = (lo0 + (0 << 64)) + (lo1 + (1 << 64))
+    assert (t0[0], t0[1]) == (total & M64, (total >> 64) & M64)
+    assert t0[2] == 2 + 3 and t0[3] == 21

@@ -113,8 +113,8 @@ def test_mgemm_raw_fuzz_vs_oracle(precision):
         bv = D.block_from_host(torch.from_numpy(np.ascontiguousarray(V.T)), n_f, 0, precision, "cuda")
         out = torch.zeros((n, m), dtype=D.torch_dtype(precision), device="cuda")
         D.mgemm_square(code, bw, bv, out, symmetric=False)
-        got = out.cpu().numpy().T
-        want = O.mgemm(W, V)
+        got = np.ascontiguousarray(out.cpu().numpy().T)
+        want = np.ascontiguousarray(O.mgemm(W, V))
         assert (got.view(np.uint8) == want.view(np.uint8)).all(), trial
         outs = torch.zeros((m, m), dtype=D.torch_dtype(precision), device="cuda")
         D.mgemm_square(code, bw, bw, outs, symmetric=True)

@@ -1,0 +1,80 @@
+"""Multi-GPU parity check (run under torchrun, one process per GPU):
+
+    torchrun --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 tools/mgpu_check.py
+
+Runs run_2way / run_3way with transport="nccl" on several grids whose rank
+count equals the world size and compares checksums with the reference's
+golden runs (tests/golden/golden.json) and with single-GPU local runs.
+Prints one JSON line per case on rank 0; exits non-zero on any mismatch.
+"""
+import json
+import os
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import paper_1705_08210_b200 as P  # noqa: E402
+
+
+def main():
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    world, rank = dist.get_world_size(), dist.get_rank()
+    gold = json.loads((ROOT / "tests" / "golden" / "golden.json").read_text())
+    bad = 0
+    cases = []
+    # golden cases (reference checksums) whose grid fits this world size
+    for c in gold["cases"]:
+        g = c["grid"]
+        if g["n_pf"] * g["n_pv"] * g["n_pr"] != world or "stage" in c or c["kind"] == "matrix":
+            continue
+        cases.append((c, None))
+    # extra grids checked against the local single-GPU run
+    extra = [
+        (2, "double", 1000, 240, dict(n_pv=world)),
+        (2, "single", 3000, 400, dict(n_pf=world)),
+        (2, "double", 777, 120, dict(n_pr=world)),
+        (3, "double", 300, 12 * world, dict(n_pv=world)),
+        (3, "single", 200, 24, dict(n_pr=world)),
+    ]
+    if world % 2 == 0:
+        extra.append((2, "double", 500, 96, dict(n_pf=2, n_pv=world // 2)))
+        extra.append((3, "double", 64, 24, dict(n_pv=2, n_pr=world // 2)))
+    for arity, prec, n_f, n_v, g in extra:
+        cases.append((dict(kind="uniform", arity=arity, precision=prec, n_f=n_f, n_v=n_v, seed=31,
+                           grid=dict(dict(n_pf=1, n_pv=1, n_pr=1, n_st=1), **g)), "local"))
+    for c, mode in cases:
+        if c["kind"] == "random-exact":
+            src = P.gen_random_exact(c["seed"], c["n_f"], c["n_v"], c["bits"])
+        elif c["kind"] == "analytic":
+            src = P.gen_analytic(0, c["n_f"], c["n_v"])
+        else:
+            src = P.gen_uniform(c["seed"], c["n_f"], c["n_v"])
+        prob = P.Problem(c["arity"], c["n_f"], c["n_v"], src, c["precision"])
+        grid = P.DecompGrid(**c["grid"])
+        run = P.run_2way if c["arity"] == 2 else P.run_3way
+        res = run(prob, grid, transport="nccl")
+        if mode == "local":
+            want = run(prob, P.DecompGrid()).checksum.hex if rank == 0 else None
+        else:
+            want = c["checksum"]
+        if rank == 0:
+            ok = res.checksum.hex == want and len(res.records) >= 0
+            bad += not ok
+            print(json.dumps({"arity": c["arity"], "precision": c["precision"], "n_f": c["n_f"],
+                              "n_v": c["n_v"], "grid": c["grid"], "checksum": res.checksum.hex,
+                              "want": want, "ok": ok, "elapsed": res.elapsed}), flush=True)
+    t = torch.tensor([bad], device="cuda")
+    dist.broadcast(t, 0)
+    dist.destroy_process_group()
+    sys.exit(1 if int(t.item()) else 0)
+
+
+if __name__ == "__main__":
+    main()
