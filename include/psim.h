@@ -47,7 +47,11 @@ extern "C" {
  * Output `vals` (may be NULL for checksum-only): diagonal task (W == V,
  * m == n): the block triangle li < lj at pair_index(li, lj, m); otherwise
  * the rectangle row-major at li * n + lj. acc[0..1] += 128-bit checksum of
- * the task (global canonical indices), acc[2] += degenerate count. */
+ * the task (global canonical indices), acc[2] += degenerate count.
+ * row_begin / row_end (row_end == 0: all rows) restrict one launch to a band
+ * of local rows (row_begin a multiple of the CTA tile height, see
+ * psim_tile_shape); positions stay those of the whole task, so consecutive
+ * bands fill consecutive segments of `vals` (used to overlap D2H with compute). */
 typedef struct psim_block2 {
   const void* W;
   int64_t ldw;
@@ -56,6 +60,7 @@ typedef struct psim_block2 {
   int64_t n_f;
   int64_t m, n;
   int32_t diagonal;
+  int64_t row_begin, row_end;
   const void* s_row; /* column sums of W's vectors (m) */
   const void* s_col; /* column sums of V's vectors (n) */
   int64_t g_row;     /* global vector id of W column 0 */
@@ -99,6 +104,8 @@ int psim_version(void);
 const char* psim_last_error(void);
 /* SM count and compute capability of the current device. */
 int psim_device_info(int* sm_count, int* cc_major, int* cc_minor);
+/* CTA output tile (rows x cols) of the min-plus kernels for a dtype. */
+int psim_tile_shape(int dtype, int* rows, int* cols);
 
 /* --- inputs ---------------------------------------------------------------- */
 /* SyntheticSpec.local_block, kind "random-exact" (verify.py:126-147):
@@ -142,7 +149,7 @@ int psim_czek2_from_numerators(int dtype, const void* N, int64_t r0, int64_t r1,
  * engine.py:197-216): dst[e] = dst[e] + src[e]. */
 int psim_fold_add(int dtype, void* dst, const void* src, int64_t count, void* stream);
 /* Output element count and CTA-tile count of a 3-way box (host-only, sync). */
-int psim_box3_plan(const psim_box3_t* box, int64_t* n_out, int64_t* n_tiles);
+int psim_box3_plan(int dtype, const psim_box3_t* box, int64_t* n_out, int64_t* n_tiles);
 /* Fused 3-way box (see psim_box3_t). */
 int psim_czek3_box(int dtype, const psim_box3_t* box, void* stream);
 

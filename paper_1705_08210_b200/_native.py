@@ -29,6 +29,7 @@ class Block2(C.Structure):
     _fields_ = [
         ("W", c_vp), ("ldw", c_i64), ("V", c_vp), ("ldv", c_i64), ("n_f", c_i64),
         ("m", c_i64), ("n", c_i64), ("diagonal", C.c_int32),
+        ("row_begin", c_i64), ("row_end", c_i64),
         ("s_row", c_vp), ("s_col", c_vp),
         ("g_row", c_i64), ("g_col", c_i64), ("n_v", c_i64),
         ("vals", c_vp), ("acc", c_vp),
@@ -58,6 +59,7 @@ SIGNATURES = {
     "psim_version": (C.c_int, []),
     "psim_last_error": (C.c_char_p, []),
     "psim_device_info": (C.c_int, [C.POINTER(C.c_int)] * 3),
+    "psim_tile_shape": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "psim_gen_random_exact": (
         C.c_int, [C.c_int, c_u64, C.c_int, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp]),
     "psim_gen_analytic": (C.c_int, [C.c_int, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp]),
@@ -75,7 +77,7 @@ SIGNATURES = {
         [C.c_int, c_vp, c_i64, c_i64, c_i64, c_i64, C.c_int, c_vp, c_vp, c_i64, c_i64, c_i64,
          c_vp, c_vp, c_vp]),
     "psim_fold_add": (C.c_int, [C.c_int, c_vp, c_vp, c_i64, c_vp]),
-    "psim_box3_plan": (C.c_int, [C.POINTER(Box3), C.POINTER(c_i64), C.POINTER(c_i64)]),
+    "psim_box3_plan": (C.c_int, [C.c_int, C.POINTER(Box3), C.POINTER(c_i64), C.POINTER(c_i64)]),
     "psim_czek3_box": (C.c_int, [C.c_int, C.POINTER(Box3), c_vp]),
     "psim_peak_minplus": (
         C.c_int, [C.c_int, C.c_int, c_i64, C.POINTER(C.c_double), C.POINTER(C.c_double), c_vp]),
@@ -118,3 +120,15 @@ def check(status: int) -> None:
 
 def call(name: str, *args) -> None:
     check(getattr(lib(), name)(*args))
+
+
+_shapes: dict = {}
+
+
+def tile_shape(code: int) -> tuple[int, int]:
+    """(rows, cols) of the min-plus CTA tile for a dtype code."""
+    if code not in _shapes:
+        r, c = C.c_int(), C.c_int()
+        call("psim_tile_shape", code, C.byref(r), C.byref(c))
+        _shapes[code] = (r.value, c.value)
+    return _shapes[code]

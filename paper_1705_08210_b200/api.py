@@ -135,8 +135,13 @@ def _result(problem, grid, transport, out, stages) -> RunResult:
 
 def run_2way(problem, grid, *, transport: str = "local", kernel: str | None = None,
              timeout: float = DEFAULT_TIMEOUT, inject_delay: float = 0.0, delay_seed: int = 0,
-             balance: str = "split", keep_values: bool = True) -> RunResult:
-    """All unique 2-way Czekanowski metrics of ``problem`` on the GPU(s)."""
+             balance: str = "split", keep_values: bool = True,
+             host_values: bool = False) -> RunResult:
+    """All unique 2-way Czekanowski metrics of ``problem`` on the GPU(s).
+
+    ``host_values=True`` streams the values into pinned host memory band by
+    band while the kernel runs (local transport), so ``records`` are ready
+    on the host when the call returns."""
     if problem.arity != 2:
         raise ConfigError(f"run_2way needs an arity-2 problem, got arity={problem.arity}")
     validate_grid(grid, problem.n_f, problem.n_v, 2)
@@ -149,7 +154,8 @@ def run_2way(problem, grid, *, transport: str = "local", kernel: str | None = No
 
         out = dist.run_2way_nccl(problem, grid, balance=balance, keep_values=keep_values)
     else:
-        out = engine2.run_local(problem, grid, balance=balance, keep_values=keep_values)
+        out = engine2.run_local(problem, grid, balance=balance, keep_values=keep_values,
+                                host_values=host_values)
     return _result(problem, grid, mode, out, None)
 
 

@@ -52,8 +52,10 @@ int check_operand(int dtype, const void* p, int64_t ld, int64_t n_f, const char*
 }
 
 // Per-pivot tile and output counts of a 3-way box (see psim_box3_t).
-void box3_counts(const psim_box3_t& b, std::vector<int64_t>* tile_pref,
+void box3_counts(int dtype, const psim_box3_t& b, std::vector<int64_t>* tile_pref,
                  std::vector<int64_t>* out_pref) {
+  int bm = 0, bn = 0;
+  psim::tile_shape(dtype, &bm, &bn);
   const int64_t nJ = b.j1 > b.j0 ? b.j1 - b.j0 : 0;
   tile_pref->assign(nJ + 1, 0);
   out_pref->assign(nJ + 1, 0);
@@ -63,7 +65,7 @@ void box3_counts(const psim_box3_t& b, std::vector<int64_t>* tile_pref,
     const int64_t klo = b.k0 > j + 1 ? b.k0 : j + 1;
     const int64_t r = ihi > b.i0 ? ihi - b.i0 : 0;
     const int64_t c = b.k1 > klo ? b.k1 - klo : 0;
-    const int64_t t = ((r + psim::kTileM - 1) / psim::kTileM) * ((c + psim::kTileN - 1) / psim::kTileN);
+    const int64_t t = ((r + bm - 1) / bm) * ((c + bn - 1) / bn);
     (*tile_pref)[jj + 1] = (*tile_pref)[jj] + (r && c ? t : 0);
     (*out_pref)[jj + 1] = (*out_pref)[jj] + r * c;
   }
@@ -85,6 +87,15 @@ int psim_device_info(int* sm_count, int* cc_major, int* cc_minor) {
   if (cc_major) cudaDeviceGetAttribute(cc_major, cudaDevAttrComputeCapabilityMajor, dev);
   if (cc_minor) cudaDeviceGetAttribute(cc_minor, cudaDevAttrComputeCapabilityMinor, dev);
   return cuda_status(cudaGetLastError(), "psim_device_info");
+}
+
+int psim_tile_shape(int dtype, int* rows, int* cols) {
+  if (int r = check_dtype(dtype)) return r;
+  int bm = 0, bn = 0;
+  psim::tile_shape(dtype, &bm, &bn);
+  if (rows) *rows = bm;
+  if (cols) *cols = bn;
+  return PSIM_OK;
 }
 
 int psim_gen_random_exact(int dtype, uint64_t seed, int bits, int64_t n_v_total, int64_t f0,
@@ -158,6 +169,12 @@ int psim_czek2_block(int dtype, const psim_block2_t* t, void* stream) {
     return fail(PSIM_ECONFIG, "diagonal task needs m == n and g_row == g_col");
   if (t->g_row < 0 || t->g_col < 0 || t->g_row + t->m > t->n_v || t->g_col + t->n > t->n_v)
     return fail(PSIM_ECONFIG, "task outside [0, n_v)");
+  int bm = 0, bn = 0;
+  psim::tile_shape(dtype, &bm, &bn);
+  const int64_t re = t->row_end ? t->row_end : t->m;
+  if (t->row_begin < 0 || re > t->m || t->row_begin > re || t->row_begin % bm)
+    return fail(PSIM_ECONFIG, "row band [%lld, %lld) invalid (begin must be a multiple of %d)",
+                (long long)t->row_begin, (long long)re, bm);
   return cuda_status(psim::czek2_block(dtype, *t, S(stream)), "psim_czek2_block");
 }
 
@@ -179,10 +196,11 @@ int psim_fold_add(int dtype, void* dst, const void* src, int64_t count, void* st
   return cuda_status(psim::fold_add(dtype, dst, src, count, S(stream)), "psim_fold_add");
 }
 
-int psim_box3_plan(const psim_box3_t* box, int64_t* n_out, int64_t* n_tiles) {
+int psim_box3_plan(int dtype, const psim_box3_t* box, int64_t* n_out, int64_t* n_tiles) {
+  if (int r = check_dtype(dtype)) return r;
   if (!box) return fail(PSIM_ECONFIG, "box is NULL");
   std::vector<int64_t> tp, op;
-  box3_counts(*box, &tp, &op);
+  box3_counts(dtype, *box, &tp, &op);
   if (n_out) *n_out = op.back();
   if (n_tiles) *n_tiles = tp.back();
   return PSIM_OK;
@@ -201,7 +219,7 @@ int psim_czek3_box(int dtype, const psim_box3_t* b, void* stream) {
       b->k1 > b->n_v)
     return fail(PSIM_ECONFIG, "box intervals outside their blocks");
   std::vector<int64_t> tp, op;
-  box3_counts(*b, &tp, &op);
+  box3_counts(dtype, *b, &tp, &op);
   const int64_t n_tiles = tp.back();
   if (n_tiles == 0) return PSIM_OK;
   cudaStream_t st = S(stream);

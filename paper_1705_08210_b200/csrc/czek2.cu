@@ -32,7 +32,10 @@ struct Args2 {
   T* out;                     // values (kCzek2), numerators (kRaw*)
   int64_t ldm;                // kRawCol leading dimension
   unsigned long long* acc;    // [3]: checksum lo, hi, degenerate count (kCzek2)
-  int64_t tiles_n;            // ceil(n / kBN) (rectangle) or tiles per edge (diagonal)
+  int64_t tiles_m, tiles_n;   // tile grid of this launch
+  int64_t row_tile0;          // first row-tile of the launch (row band)
+  int64_t m_end;              // rows >= m_end are outside the band
+  const int64_t* row_pref;    // diagonal tasks: tiles before each row-tile (device)
 };
 
 // Position of local pair (i, j) in the packed layout shared by values and
@@ -43,37 +46,38 @@ __device__ __forceinline__ int64_t packed_pos(int diagonal, int64_t i, int64_t j
   return diagonal ? (int64_t)pair_index(i, j, m) : i * n + j;
 }
 
-template <typename T, int MODE>
-__global__ void __launch_bounds__(kNT, 1) k_minplus2(const Args2<T> a) {
+template <class C, int MODE>
+__global__ void __launch_bounds__(kNT, C::MINB) k_minplus2(const Args2<typename C::T> a) {
+  using T = typename C::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* smem = reinterpret_cast<T*>(smem_raw);
   int bi, bj;
   if (a.diagonal) {
-    tri_tile((int64_t)blockIdx.x, a.tiles_n, bi, bj);
+    diag_tile((int64_t)blockIdx.x, a.row_pref, a.tiles_m, a.row_tile0, C::BM, C::BN, bi, bj);
   } else {
-    bi = (int)(blockIdx.x / a.tiles_n);
+    bi = (int)(a.row_tile0 + blockIdx.x / a.tiles_n);
     bj = (int)(blockIdx.x % a.tiles_n);
   }
-  const int64_t row0 = (int64_t)bi * kBM, col0 = (int64_t)bj * kBN;
-  const int rows = (int)min64(kBM, a.m - row0);
-  const int cols = (int)min64(kBN, a.n - col0);
+  const int64_t row0 = (int64_t)bi * C::BM, col0 = (int64_t)bj * C::BN;
+  const int rows = (int)min64(C::BM, a.m_end - row0);
+  const int cols = (int)min64(C::BN, a.n - col0);
 
-  T acc[kTM][kTN];
-  minplus_tile<T, false>(a.W + row0 * a.ldw, a.ldw, rows, a.V + col0 * a.ldv, a.ldv, cols,
+  T acc[C::TM][C::TN];
+  minplus_tile<C, false>(a.W + row0 * a.ldw, a.ldw, rows, a.V + col0 * a.ldv, a.ldv, cols,
                          nullptr, a.n_f, acc, smem);
 
   const int ty = thread_ty(), tx = thread_tx();
   if (MODE == kCzek2) {
     Cks c;
 #pragma unroll
-    for (int mi = 0; mi < kTM; ++mi) {
+    for (int mi = 0; mi < C::TM; ++mi) {
       const int li = ty + 16 * mi;
       if (li >= rows) continue;
       const int64_t i = row0 + li;
       const T si = a.s_row[i];
       const uint64_t gi = (uint64_t)(a.g_row + i);
 #pragma unroll
-      for (int nj = 0; nj < kTN; ++nj) {
+      for (int nj = 0; nj < C::TN; ++nj) {
         const int lj = tx + 16 * nj;
         const int64_t j = col0 + lj;
         if (lj >= cols || (a.diagonal && j <= i)) continue;
@@ -90,12 +94,12 @@ __global__ void __launch_bounds__(kNT, 1) k_minplus2(const Args2<T> a) {
     cks_block_flush<kNT>(a.acc, c);
   } else {
 #pragma unroll
-    for (int mi = 0; mi < kTM; ++mi) {
+    for (int mi = 0; mi < C::TM; ++mi) {
       const int li = ty + 16 * mi;
       if (li >= rows) continue;
       const int64_t i = row0 + li;
 #pragma unroll
-      for (int nj = 0; nj < kTN; ++nj) {
+      for (int nj = 0; nj < C::TN; ++nj) {
         const int lj = tx + 16 * nj;
         const int64_t j = col0 + lj;
         if (lj >= cols) continue;
@@ -110,6 +114,118 @@ __global__ void __launch_bounds__(kNT, 1) k_minplus2(const Args2<T> a) {
       }
     }
   }
+}
+
+// Row-tile prefix of a diagonal task's tile grid (see diag_tile): one CTA,
+// each thread folds a contiguous range of row-tiles, then a block scan.
+__global__ void __launch_bounds__(1024) k_diag_prefix(int64_t tiles_m, int64_t row_tile0,
+                                                      int64_t tiles_n, int64_t bm, int64_t bn,
+                                                      int64_t* __restrict__ pref) {
+  __shared__ int64_t s[1024];
+  const int64_t per = (tiles_m + blockDim.x - 1) / blockDim.x;
+  const int64_t a = min64(tiles_m, threadIdx.x * per), e = min64(tiles_m, a + per);
+  auto count = [&](int64_t b) {
+    return max64(0, tiles_n - ((row_tile0 + b) * bm + 1) / bn);
+  };
+  int64_t sum = 0;
+  for (int64_t b = a; b < e; ++b) sum += count(b);
+  s[threadIdx.x] = sum;
+  __syncthreads();
+  for (int off = 1; off < (int)blockDim.x; off <<= 1) {
+    const int64_t v = threadIdx.x >= off ? s[threadIdx.x - off] : 0;
+    __syncthreads();
+    s[threadIdx.x] += v;
+    __syncthreads();
+  }
+  int64_t run = threadIdx.x ? s[threadIdx.x - 1] : 0;
+  for (int64_t b = a; b < e; ++b) {
+    pref[b] = run;
+    run += count(b);
+  }
+  if (threadIdx.x == blockDim.x - 1) pref[tiles_m] = s[threadIdx.x];
+}
+
+template <class C>
+static int64_t diag_tiles(int64_t tiles_m, int64_t row_tile0, int64_t tiles_n) {
+  int64_t t = 0;
+  for (int64_t b = row_tile0; b < row_tile0 + tiles_m; ++b) {
+    const int64_t c = tiles_n - (b * C::BM + 1) / C::BN;
+    t += c > 0 ? c : 0;
+  }
+  return t;
+}
+
+// Launch rows [row_begin, row_end) of a task (row_begin % BM == 0).
+template <class C, int MODE>
+static cudaError_t launch2(Args2<typename C::T> a, cudaStream_t st, int64_t row_begin = 0,
+                           int64_t row_end = 0) {
+  cudaError_t e = cudaFuncSetAttribute(k_minplus2<C, MODE>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  if (row_end <= 0) row_end = a.m;
+  if (a.m <= 0 || a.n <= 0 || row_end <= row_begin) return cudaSuccess;
+  a.row_tile0 = row_begin / C::BM;
+  a.m_end = row_end;
+  a.tiles_m = (row_end - row_begin + C::BM - 1) / C::BM;
+  a.tiles_n = (a.n + C::BN - 1) / C::BN;
+  int64_t blocks;
+  int64_t* pref = nullptr;
+  if (a.diagonal) {
+    blocks = diag_tiles<C>(a.tiles_m, a.row_tile0, a.tiles_n);
+    e = cudaMallocAsync(&pref, (a.tiles_m + 1) * sizeof(int64_t), st);
+    if (e != cudaSuccess) return e;
+    k_diag_prefix<<<1, 1024, 0, st>>>(a.tiles_m, a.row_tile0, a.tiles_n, C::BM, C::BN, pref);
+    a.row_pref = pref;
+  } else {
+    blocks = a.tiles_m * a.tiles_n;
+  }
+  if (blocks > 0x7fffffffLL) e = cudaErrorInvalidConfiguration;
+  else if (blocks > 0) k_minplus2<C, MODE><<<(unsigned)blocks, kNT, C::SMEM_BYTES, st>>>(a);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (pref) {
+    cudaError_t e2 = cudaFreeAsync(pref, st);
+    if (e == cudaSuccess) e = e2;
+  }
+  return e;
+}
+
+template <typename T>
+static Args2<T> make_args(const void* W, int64_t ldw, const void* V, int64_t ldv, int64_t n_f,
+                          int64_t m, int64_t n, int diagonal) {
+  Args2<T> a{};
+  a.W = static_cast<const T*>(W);
+  a.ldw = ldw;
+  a.V = static_cast<const T*>(V);
+  a.ldv = ldv;
+  a.n_f = n_f;
+  a.m = m;
+  a.n = n;
+  a.diagonal = diagonal;
+  return a;
+}
+
+template <typename T>
+cudaError_t czek2_block_t(const Czek2Block& t, cudaStream_t st) {
+  Args2<T> a = make_args<T>(t.W, t.ldw, t.V, t.ldv, t.n_f, t.m, t.n, t.diagonal);
+  a.s_row = static_cast<const T*>(t.s_row);
+  a.s_col = static_cast<const T*>(t.s_col);
+  a.g_row = t.g_row;
+  a.g_col = t.g_col;
+  a.n_v = t.n_v;
+  a.out = static_cast<T*>(t.vals);
+  a.acc = t.acc;
+  return launch2<typename Prod<T>::C, kCzek2>(a, st, t.row_begin, t.row_end);
+}
+
+template <typename T>
+cudaError_t mgemm_t(const void* W, int64_t ldw, const void* V, int64_t ldv, int64_t n_f,
+                    int64_t m, int64_t n, int symmetric, void* M, int64_t ldm, int packed,
+                    cudaStream_t st) {
+  Args2<T> a = make_args<T>(W, ldw, V, ldv, n_f, m, n, symmetric);
+  a.out = static_cast<T*>(M);
+  a.ldm = ldm;
+  using C = typename Prod<T>::C;
+  return packed ? launch2<C, kRawPacked>(a, st) : launch2<C, kRawCol>(a, st);
 }
 
 // Values + checksum from already-reduced packed numerators (the field-axis
@@ -142,64 +258,6 @@ __global__ void __launch_bounds__(256) k_czek2_from_num(const T* __restrict__ N,
     c.deg += zero ? 1ull : 0ull;
   }
   cks_block_flush<256>(acc, c);
-}
-
-template <typename T, int MODE>
-static cudaError_t launch2(const Args2<T>& a, cudaStream_t st) {
-  using TL = Tile<T>;
-  cudaError_t e = cudaFuncSetAttribute(k_minplus2<T, MODE>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, TL::SMEM_BYTES);
-  if (e != cudaSuccess) return e;
-  if (a.m <= 0 || a.n <= 0) return cudaSuccess;
-  int64_t blocks;
-  if (a.diagonal) {
-    const int64_t T_ = a.tiles_n;
-    blocks = T_ * (T_ + 1) / 2;
-  } else {
-    blocks = ((a.m + kBM - 1) / kBM) * a.tiles_n;
-  }
-  if (blocks > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-  k_minplus2<T, MODE><<<(unsigned)blocks, kNT, TL::SMEM_BYTES, st>>>(a);
-  return cudaGetLastError();
-}
-
-template <typename T>
-static Args2<T> make_args(const void* W, int64_t ldw, const void* V, int64_t ldv, int64_t n_f,
-                          int64_t m, int64_t n, int diagonal) {
-  Args2<T> a{};
-  a.W = static_cast<const T*>(W);
-  a.ldw = ldw;
-  a.V = static_cast<const T*>(V);
-  a.ldv = ldv;
-  a.n_f = n_f;
-  a.m = m;
-  a.n = n;
-  a.diagonal = diagonal;
-  a.tiles_n = (n + kBN - 1) / kBN;
-  return a;
-}
-
-template <typename T>
-cudaError_t czek2_block_t(const Czek2Block& t, cudaStream_t st) {
-  Args2<T> a = make_args<T>(t.W, t.ldw, t.V, t.ldv, t.n_f, t.m, t.n, t.diagonal);
-  a.s_row = static_cast<const T*>(t.s_row);
-  a.s_col = static_cast<const T*>(t.s_col);
-  a.g_row = t.g_row;
-  a.g_col = t.g_col;
-  a.n_v = t.n_v;
-  a.out = static_cast<T*>(t.vals);
-  a.acc = t.acc;
-  return launch2<T, kCzek2>(a, st);
-}
-
-template <typename T>
-cudaError_t mgemm_t(const void* W, int64_t ldw, const void* V, int64_t ldv, int64_t n_f,
-                    int64_t m, int64_t n, int symmetric, void* M, int64_t ldm, int packed,
-                    cudaStream_t st) {
-  Args2<T> a = make_args<T>(W, ldw, V, ldv, n_f, m, n, symmetric);
-  a.out = static_cast<T*>(M);
-  a.ldm = ldm;
-  return packed ? launch2<T, kRawPacked>(a, st) : launch2<T, kRawCol>(a, st);
 }
 
 template <typename T>

@@ -27,10 +27,11 @@
 
 namespace psim {
 
-template <typename T>
-__global__ void __launch_bounds__(kNT, 1)
+template <class C>
+__global__ void __launch_bounds__(kNT, C::MINB)
     k_czek3(const Czek3Box b, const int64_t* __restrict__ tile_pref,
             const int64_t* __restrict__ out_pref, int64_t nJ) {
+  using T = typename C::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* smem = reinterpret_cast<T*>(smem_raw);
 
@@ -45,12 +46,12 @@ __global__ void __launch_bounds__(kNT, 1)
   const int64_t ihi = min64(b.i1, j);
   const int64_t klo = max64(b.k0, j + 1);
   const int64_t nrows = ihi - b.i0, ncols = b.k1 - klo;
-  const int64_t tiles_k = (ncols + kBN - 1) / kBN;
+  const int64_t tiles_k = (ncols + C::BN - 1) / C::BN;
   const int64_t lt = t - tile_pref[lo];
   const int64_t ti = lt / tiles_k, tk = lt - ti * tiles_k;
-  const int64_t r0 = ti * kBM, c0 = tk * kBN;
-  const int rows = (int)min64(kBM, nrows - r0);
-  const int cols = (int)min64(kBN, ncols - c0);
+  const int64_t r0 = ti * C::BM, c0 = tk * C::BN;
+  const int rows = (int)min64(C::BM, nrows - r0);
+  const int cols = (int)min64(C::BN, ncols - c0);
 
   const T* VA = static_cast<const T*>(b.VA);
   const T* VB = static_cast<const T*>(b.VB);
@@ -59,8 +60,8 @@ __global__ void __launch_bounds__(kNT, 1)
   const int64_t kc = klo - b.c0 + c0;    // local column of the tile's first k in block C
   const int64_t jb = j - b.b0;           // local column of j in block B
 
-  T acc[kTM][kTN];
-  minplus_tile<T, true>(VA + ia * b.ldA, b.ldA, rows, VC + kc * b.ldC, b.ldC, cols,
+  T acc[C::TM][C::TN];
+  minplus_tile<C, true>(VA + ia * b.ldA, b.ldA, rows, VC + kc * b.ldC, b.ldC, cols,
                         VB + jb * b.ldB, b.n_f, acc, smem);
 
   const T* SA = static_cast<const T*>(b.SA);
@@ -77,7 +78,7 @@ __global__ void __launch_bounds__(kNT, 1)
   const int ty = thread_ty(), tx = thread_tx();
   Cks c;
 #pragma unroll
-  for (int mi = 0; mi < kTM; ++mi) {
+  for (int mi = 0; mi < C::TM; ++mi) {
     const int li = ty + 16 * mi;
     if (li >= rows) continue;
     const int64_t ai = ia + li;            // local in A
@@ -90,7 +91,7 @@ __global__ void __launch_bounds__(kNT, 1)
                              pair_index((uint64_t)(j - i - 1), (uint64_t)(j - i), nv - (uint64_t)i - 1);
     const int64_t orow = obase + (r0 + li) * ncols + c0;
 #pragma unroll
-    for (int nk = 0; nk < kTN; ++nk) {
+    for (int nk = 0; nk < C::TN; ++nk) {
       const int lk = tx + 16 * nk;
       if (lk >= cols) continue;
       const int64_t kcl = kc + lk;          // local in C
@@ -112,7 +113,7 @@ __global__ void __launch_bounds__(kNT, 1)
 // Per-pivot prefix sums of CTA tiles and output elements for a box, one CTA:
 // each thread folds a contiguous j range, then a block scan of the partials.
 __global__ void __launch_bounds__(1024) k_box3_prefix(int64_t i0, int64_t i1, int64_t j0,
-                                                      int64_t j1, int64_t k0, int64_t k1,
+                                                      int64_t j1, int64_t k0, int64_t k1, int64_t bm, int64_t bn,
                                                       int64_t* __restrict__ tile_pref,
                                                       int64_t* __restrict__ out_pref) {
   __shared__ int64_t s_t[1024], s_o[1024];
@@ -123,7 +124,7 @@ __global__ void __launch_bounds__(1024) k_box3_prefix(int64_t i0, int64_t i1, in
     const int64_t j = j0 + jj;
     const int64_t r = max64(0, min64(i1, j) - i0);
     const int64_t c = max64(0, k1 - max64(k0, j + 1));
-    t = ((r + kBM - 1) / kBM) * ((c + kBN - 1) / kBN);
+    t = ((r + bm - 1) / bm) * ((c + bn - 1) / bn);
     o = r * c;
   };
   int64_t st = 0, so = 0;
@@ -162,18 +163,28 @@ __global__ void __launch_bounds__(1024) k_box3_prefix(int64_t i0, int64_t i1, in
 
 template <typename T>
 static cudaError_t czek3_t(const Czek3Box& b, int64_t* work, int64_t n_tiles, cudaStream_t st) {
-  using TL = Tile<T>;
-  cudaError_t e = cudaFuncSetAttribute(k_czek3<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       TL::SMEM_BYTES);
+  using C = typename Prod<T>::C;
+  cudaError_t e = cudaFuncSetAttribute(k_czek3<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       C::SMEM_BYTES);
   if (e != cudaSuccess) return e;
   if (n_tiles <= 0) return cudaSuccess;
   if (n_tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
   const int64_t nJ = b.j1 - b.j0;
   int64_t* tp = work;
   int64_t* op = work + nJ + 1;
-  k_box3_prefix<<<1, 1024, 0, st>>>(b.i0, b.i1, b.j0, b.j1, b.k0, b.k1, tp, op);
-  k_czek3<T><<<(unsigned)n_tiles, kNT, TL::SMEM_BYTES, st>>>(b, tp, op, nJ);
+  k_box3_prefix<<<1, 1024, 0, st>>>(b.i0, b.i1, b.j0, b.j1, b.k0, b.k1, C::BM, C::BN, tp, op);
+  k_czek3<C><<<(unsigned)n_tiles, kNT, C::SMEM_BYTES, st>>>(b, tp, op, nJ);
   return cudaGetLastError();
+}
+
+void tile_shape(int dtype, int* bm, int* bn) {
+  if (dtype == kF64) {
+    *bm = Prod<double>::C::BM;
+    *bn = Prod<double>::C::BN;
+  } else {
+    *bm = Prod<float>::C::BM;
+    *bn = Prod<float>::C::BN;
+  }
 }
 
 cudaError_t czek3_box(int dtype, const Czek3Box& b, int64_t* d_work, int64_t n_tiles,

@@ -14,37 +14,51 @@ namespace psim {
 
 constexpr int kPeakAcc = 16;
 
+// Two banks of accumulators: each half-iteration updates one bank with min
+// operands read from the other bank, so both operands are per-thread vector
+// registers that change every iteration (nothing can be hoisted) while every
+// dependency is >= 16 instructions away (no latency stall) -- the register
+// traffic of the real mainloop, whose operands come from LDS.
+// VAR 2 makes one operand CTA-uniform (fewer register-file reads): an
+// optimistic bound, reported for reference only.
+template <typename T>
+__device__ __forceinline__ void peak_bank(T (&dst)[kPeakAcc], const T (&src)[kPeakAcc], T y0,
+                                          T y1, bool uniform, bool packed) {
+#pragma unroll
+  for (int k = 0; k < kPeakAcc; k += 2) {
+    const T a0 = src[k], a1 = src[k + 1];
+    const T b0 = uniform ? y0 : src[(k + 5) % kPeakAcc];
+    const T b1 = uniform ? y1 : src[(k + 11) % kPeakAcc];
+    if (sizeof(T) == 4 && packed) {
+      fadd2(*reinterpret_cast<float*>(&dst[k]), *reinterpret_cast<float*>(&dst[k + 1]),
+            fminf((float)a0, (float)b0), fminf((float)a1, (float)b1));
+    } else {
+      dst[k] = Traits<T>::add(dst[k], Traits<T>::min(a0, b0));
+      dst[k + 1] = Traits<T>::add(dst[k + 1], Traits<T>::min(a1, b1));
+    }
+  }
+}
+
 template <typename T, int VAR>
 __global__ void __launch_bounds__(256) k_peak(int64_t iters, T seed, T* sink, long long* cycles) {
-  T acc[kPeakAcc];
+  T acc[kPeakAcc], bcc[kPeakAcc];
 #pragma unroll
-  for (int k = 0; k < kPeakAcc; ++k) acc[k] = seed * T(k + threadIdx.x % 7);
+  for (int k = 0; k < kPeakAcc; ++k) {
+    acc[k] = seed * T(k + threadIdx.x % 7);
+    bcc[k] = seed * T(2 * k + 1 + threadIdx.x % 5);
+  }
   const T y0 = seed * T(3), y1 = seed * T(5);
   __syncthreads();
   const long long c0 = clock64();
   for (int64_t it = 0; it < iters; ++it) {
-#pragma unroll
-    for (int k = 0; k < kPeakAcc; k += 2) {
-      // Both min operands are per-thread vector registers that change every
-      // iteration (other accumulators), as in the mainloop where they come
-      // from LDS; VAR 2 uses a CTA-uniform operand (an optimistic bound).
-      const T u0 = VAR == 2 ? y0 : acc[(k + 5) % kPeakAcc];
-      const T u1 = VAR == 2 ? y1 : acc[(k + 11) % kPeakAcc];
-      if (sizeof(T) == 4 && VAR != 1) {
-        fadd2(*reinterpret_cast<float*>(&acc[k]), *reinterpret_cast<float*>(&acc[k + 1]),
-              fminf((float)acc[(k + 3) % kPeakAcc], (float)u0),
-              fminf((float)acc[(k + 6) % kPeakAcc], (float)u1));
-      } else {
-        acc[k] = Traits<T>::add(acc[k], Traits<T>::min(acc[(k + 3) % kPeakAcc], u0));
-        acc[k + 1] = Traits<T>::add(acc[k + 1], Traits<T>::min(acc[(k + 6) % kPeakAcc], u1));
-      }
-    }
+    peak_bank<T>(acc, bcc, y0, y1, VAR == 2, VAR != 1);
+    peak_bank<T>(bcc, acc, y0, y1, VAR == 2, VAR != 1);
   }
   __syncthreads();
   const long long c1 = clock64();
   T s = T(0);
 #pragma unroll
-  for (int k = 0; k < kPeakAcc; ++k) s += acc[k];
+  for (int k = 0; k < kPeakAcc; ++k) s += acc[k] + bcc[k];
   if (s == T(-1)) sink[threadIdx.x] = s;  // never true; keeps the loop live
   if (threadIdx.x == 0) cycles[blockIdx.x] = c1 - c0;
 }
@@ -80,7 +94,7 @@ static cudaError_t peak_t(int64_t iters, double* cmp_per_s, double* cmp_per_clk_
   long long cmax = 0;
   for (int b = 0; b < blocks; ++b) cmax = h[b] > cmax ? h[b] : cmax;
   delete[] h;
-  const double cmps = (double)blocks * 256.0 * (double)iters * kPeakAcc;
+  const double cmps = (double)blocks * 256.0 * (double)iters * 2 * kPeakAcc;
   *cmp_per_s = cmps / (ms * 1e-3);
   *cmp_per_clk_sm = cmps / (double)sms / (double)cmax;
   cudaFreeAsync(sink, st);

@@ -12,9 +12,9 @@ namespace psim {
 constexpr int kF32 = 0;
 constexpr int kF64 = 1;
 
-// CTA output tile of the min-plus kernels (rows x cols).
-constexpr int kTileM = 128;
-constexpr int kTileN = 128;
+// CTA output tile (rows x cols) of the production min-plus kernels per dtype
+// (defined from the tile configurations in minplus.cuh).
+void tile_shape(int dtype, int* bm, int* bn);
 
 // The public task descriptors double as the internal ones.
 using Czek2Block = psim_block2_t;

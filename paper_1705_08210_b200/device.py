@@ -146,10 +146,13 @@ def acc_words(acc: torch.Tensor) -> tuple[int, int, int]:
 
 def czek2_block(code: int, W: Block, r0: int, r1: int, V: Block, c0: int, c1: int,
                 s_row: torch.Tensor, s_col: torch.Tensor, diagonal: bool, n_v: int,
-                vals: torch.Tensor | None, acc: torch.Tensor) -> None:
+                vals: torch.Tensor | None, acc: torch.Tensor, band: tuple[int, int] = (0, 0)
+                ) -> None:
+    """One fused 2-way task; ``band`` = task-local rows [begin, end) of this launch."""
     t = N.Block2(
         W=W.col_ptr(r0), ldw=W.ld, V=V.col_ptr(c0), ldv=V.ld, n_f=W.n_fp,
         m=r1 - r0, n=c1 - c0, diagonal=1 if diagonal else 0,
+        row_begin=band[0], row_end=band[1],
         s_row=s_row.data_ptr() + r0 * s_row.element_size(),
         s_col=s_col.data_ptr() + c0 * s_col.element_size(),
         g_row=W.v0 + r0, g_col=V.v0 + c0, n_v=n_v,
@@ -173,6 +176,32 @@ def mgemm_square(code: int, W: Block, V: Block, out: torch.Tensor, symmetric: bo
 
 def pair_count(m: int, n: int, diagonal: bool) -> int:
     return m * (m - 1) // 2 if diagonal else m * n
+
+
+def packed_offset(row: int, m: int, n: int, diagonal: bool) -> int:
+    """Start of task-local row `row` in the packed layout (triangle / rectangle)."""
+    return row * (2 * m - row - 1) // 2 if diagonal else row * n
+
+
+def row_bands(m: int, n: int, diagonal: bool, parts: int, align: int) -> list[tuple[int, int]]:
+    """Cut rows [0, m) into <= `parts` bands of about equal element count whose
+    starts are multiples of `align` (the kernel's CTA tile height)."""
+    total = pair_count(m, n, diagonal)
+    bounds = [0]
+    for p in range(1, parts):
+        target = total * p / parts
+        lo, hi = bounds[-1], m
+        while lo < hi:  # first row whose packed start reaches the target
+            mid = (lo + hi) // 2
+            if packed_offset(mid, m, n, diagonal) < target:
+                lo = mid + 1
+            else:
+                hi = mid
+        b = (lo // align) * align
+        if b > bounds[-1]:
+            bounds.append(b)
+    bounds.append(m)
+    return [(bounds[i], bounds[i + 1]) for i in range(len(bounds) - 1) if bounds[i + 1] > bounds[i]]
 
 
 def dtype_np(precision: str):

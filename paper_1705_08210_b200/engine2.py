@@ -21,6 +21,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
+from . import _native as N
 from . import device as D
 from .domain import RankCoords, n_ranks
 from .plan import Task2, plan_2way
@@ -48,16 +49,50 @@ def fold_sums(parts: list[torch.Tensor], code: int) -> torch.Tensor:
     return total
 
 
+class HostSink:
+    """Streams finished row bands of device values into pinned host memory on a
+    side stream, overlapping the D2H copy with the next band's kernel.
+    Pinned buffers come from torch's caching host allocator (reused once the
+    previous result is released)."""
+
+    def __init__(self, bands: int = 8):
+        self.bands = bands
+        self.stream = torch.cuda.Stream()
+
+    def buffer(self, count: int, dtype) -> torch.Tensor:
+        return torch.empty(count, dtype=dtype, pin_memory=True)
+
+    def copy(self, host: torch.Tensor, dev: torch.Tensor, a: int, b: int) -> None:
+        ev = torch.cuda.Event()
+        ev.record()
+        self.stream.wait_event(ev)
+        with torch.cuda.stream(self.stream):
+            host[a:b].copy_(dev[a:b], non_blocking=True)
+        dev.record_stream(self.stream)
+
+    def finish(self) -> None:
+        self.stream.synchronize()
+
+
 def run_task(code: int, problem, grid, task: Task2, row_blocks: list, col_blocks: list,
              s_row: torch.Tensor, s_col: torch.Tensor, acc: torch.Tensor,
-             keep_values: bool) -> PairPiece:
+             keep_values: bool, sink: HostSink | None = None) -> PairPiece:
     """One Task2 over field-slab lists row_blocks[p_f] / col_blocks[p_f]."""
     m, n = task.r1 - task.r0, task.c1 - task.c0
     count = D.pair_count(m, n, task.diagonal)
     dev = acc.device
     tdt = D.torch_dtype(problem.precision)
-    vals = torch.empty(count, dtype=tdt, device=dev) if keep_values else None
+    vals = torch.empty(count, dtype=tdt, device=dev) if keep_values or sink else None
     W0, V0 = row_blocks[0], col_blocks[0]
+    if len(row_blocks) == 1 and sink is not None:
+        host = sink.buffer(count, tdt)
+        bm, _ = N.tile_shape(code)
+        for a, b in D.row_bands(m, n, task.diagonal, sink.bands, bm):
+            D.czek2_block(code, W0, task.r0, task.r1, V0, task.c0, task.c1, s_row, s_col,
+                          task.diagonal, problem.n_v, vals, acc, band=(a, b))
+            sink.copy(host, vals, D.packed_offset(a, m, n, task.diagonal),
+                      D.packed_offset(b, m, n, task.diagonal))
+        return PairPiece(W0.v0 + task.r0, V0.v0 + task.c0, m, n, task.diagonal, 0, m, host)
     if len(row_blocks) == 1:
         D.czek2_block(code, W0, task.r0, task.r1, V0, task.c0, task.c1, s_row, s_col,
                       task.diagonal, problem.n_v, vals, acc)
@@ -71,6 +106,10 @@ def run_task(code: int, problem, grid, task: Task2, row_blocks: list, col_blocks
         finish_numerators(code, total, 0, m, m, n, task.diagonal,
                           s_row[task.r0:], s_col[task.c0:], W0.v0 + task.r0, V0.v0 + task.c0,
                           problem.n_v, vals, acc)
+        if sink is not None:
+            host = sink.buffer(count, tdt)
+            sink.copy(host, vals, 0, count)
+            vals = host
     return PairPiece(W0.v0 + task.r0, V0.v0 + task.c0, m, n, task.diagonal, 0, m, vals)
 
 
@@ -82,8 +121,10 @@ def finish_numerators(code, N, r0, r1, m, n, diagonal, s_row, s_col, g_row, g_co
              D.stream_ptr())
 
 
-def run_local(problem, grid, balance: str = "split", keep_values: bool = True) -> Outcome:
+def run_local(problem, grid, balance: str = "split", keep_values: bool = True,
+              host_values: bool = False) -> Outcome:
     dev = torch.device("cuda", torch.cuda.current_device())
+    sink = HostSink() if host_values else None
     code = D.code_of(problem.precision)
     n_vp = problem.n_v // grid.n_pv
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -105,11 +146,13 @@ def run_local(problem, grid, balance: str = "split", keep_values: bool = True) -
                 rows = [blocks[p_f, ev.row_block] for p_f in range(grid.n_pf)]
                 cols = [blocks[p_f, ev.col_block] for p_f in range(grid.n_pf)]
                 piece = run_task(code, problem, grid, ev, rows, cols, sums[ev.row_block],
-                                 sums[ev.col_block], acc, keep_values)
+                                 sums[ev.col_block], acc, keep_values, sink)
                 pieces.append(piece)
                 count += D.pair_count(piece.m, piece.n, piece.diagonal)
     end.record()
     end.synchronize()
+    if sink is not None:
+        sink.finish()
     lo, hi, deg = D.acc_words(acc)
     all_sums = torch.cat([sums[p] for p in range(grid.n_pv)]).cpu().numpy()
     return Outcome(pieces, lo, hi, deg, count, all_sums, start.elapsed_time(end) * 1e-3)

@@ -40,9 +40,9 @@ def box_struct(box: Box, blocks: dict, sums: dict, tables, n_f: int, n_v: int,
     )
 
 
-def box_plan(b: N.Box3) -> tuple[int, int]:
+def box_plan(b: N.Box3, code: int = N.F64) -> tuple[int, int]:
     n_out, n_tiles = C.c_int64(), C.c_int64()
-    N.call("psim_box3_plan", C.byref(b), C.byref(n_out), C.byref(n_tiles))
+    N.call("psim_box3_plan", code, C.byref(b), C.byref(n_out), C.byref(n_tiles))
     return n_out.value, n_tiles.value
 
 

@@ -65,6 +65,6 @@ def test_box3_plan_counts_match_host_plan(lib):
                 Box((0, 1, 2), 5, 17, 20, 40, 40, 60), Box((0, 0, 0), 0, 300, 0, 300, 250, 300)):
         b = N.Box3(i0=box.i0, i1=box.i1, j0=box.j0, j1=box.j1, k0=box.k0, k1=box.k1)
         n_out, n_tiles = C.c_int64(), C.c_int64()
-        assert lib.psim_box3_plan(C.byref(b), C.byref(n_out), C.byref(n_tiles)) == 0
+        assert lib.psim_box3_plan(1, C.byref(b), C.byref(n_out), C.byref(n_tiles)) == 0
         assert n_out.value == box_count(box)
         assert n_tiles.value > 0
