@@ -214,7 +214,9 @@ def run_ours(args) -> dict | None:
     log(f"[bench] min+add peak {precision}: {peak:.4e} cmp/s ({peak_clk:.2f} cmp/clk/SM, "
         f"variant {peak_var})")
 
-    grid = P.DecompGrid(n_pv=world) if arity == 2 else P.DecompGrid(n_pv=world)
+    # cfg5 is the field-axis split (n_pf = N, NCCL ordered reduce-scatter of
+    # partial numerators); every other config splits the vector axis.
+    grid = P.DecompGrid(n_pf=world) if args.config == "cfg5" else P.DecompGrid(n_pv=world)
     spec = P.gen_random_exact(SEED, n_f, n_v, bits)
     prob = P.Problem(arity, n_f, n_v, spec, precision)
 
@@ -291,7 +293,10 @@ def run_ours(args) -> dict | None:
             "config": {
                 "workload": desc, "arity": arity, "num_field": n_f, "num_vector": n_v,
                 "comparisons_per_step": total_cmp,
-                "parallelism": f"circulant n_pv={world}" if world > 1 else "single slab",
+                "parallelism": ("single slab" if world == 1 else
+                                f"field split n_pf={world}" if args.config == "cfg5" else
+                                f"circulant n_pv={world}" if arity == 2 else
+                                f"tetrahedral n_pv={world}"),
                 "l2": "inputs > 126 MB L2 (no flush needed)",
                 "checksum": cks,
             },
@@ -420,7 +425,17 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
-    line = run_reference(args) if args.impl == "reference" else run_ours(args)
+    # Keep stdout to the single JSON line: libraries (NCCL's version banner,
+    # torch warnings) write to fd 1, so point fd 1 at stderr while running.
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        line = run_reference(args) if args.impl == "reference" else run_ours(args)
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved, 1)
+        os.close(saved)
     if line is not None:
         print(json.dumps(line), flush=True)
 

@@ -152,6 +152,15 @@ int psim_fold_add(int dtype, void* dst, const void* src, int64_t count, void* st
 int psim_box3_plan(int dtype, const psim_box3_t* box, int64_t* n_out, int64_t* n_tiles);
 /* Fused 3-way box (see psim_box3_t). */
 int psim_czek3_box(int dtype, const psim_box3_t* box, void* stream);
+/* Field-axis path of a box (metrics3.py:163-164): n_ijk = sum_q min(min(x_j, v_i), v_k)
+ * over this rank's field slab, written to box->vals (pivot-major, no values,
+ * no checksum); sums / tables / acc may be NULL. */
+int psim_czek3_box_numerators(int dtype, const psim_box3_t* box, void* stream);
+/* Values + checksum (into box->acc) of elements [e0, e1) of a box's
+ * pivot-major layout from folded n_ijk (n3, vals point at element e0);
+ * box->SA..NBC must hold the folded sums and numerator tables. */
+int psim_czek3_from_numerators(int dtype, const psim_box3_t* box, const void* n3, int64_t e0,
+                               int64_t e1, void* vals, void* stream);
 
 /* --- measurement ----------------------------------------------------------- */
 /* Min+add issue-rate microbenchmark of the mainloop mix (roofline

@@ -173,6 +173,39 @@ def checksum_hex(canonical_indices, vals) -> str:
     return format(checksum(canonical_indices, vals), "032x")
 
 
+def values_field_split(V, arity: int, n_pf: int):
+    """Values of a run whose field axis is split into n_pf slabs: every
+    numerator and column sum is a per-slab sequential sum, folded in
+    ascending p_f order (engine.py:197-216; metrics2.py:135-156,
+    metrics3.py:88-164)."""
+    V = np.asarray(V)
+    dt = V.dtype.type
+    w = V.shape[0] // n_pf
+    slabs = [V[p * w:(p + 1) * w] for p in range(n_pf)]
+
+    def fold(parts):
+        total = parts[0]
+        for p in parts[1:]:
+            total = total + p
+        return total
+
+    N = fold([mgemm(s, s) for s in slabs])
+    s = fold([column_sums(x) for x in slabs])
+    if arity == 2:
+        iu, ju = np.triu_indices(V.shape[1], k=1)
+        d = s[iu] + s[ju]
+        zero = d == 0
+        vals = (dt(2) * N[iu, ju]) / np.where(zero, dt(1), d)
+        return np.where(zero, dt(0), vals).astype(V.dtype), zero
+    T = fold([triple_min(x) for x in slabs])
+    i, j, k = triple_ids(V.shape[1])
+    n3 = ((N[i, j] + N[i, k]) + N[j, k]) - T[i, j, k]
+    d = (s[i] + s[j]) + s[k]
+    zero = d == 0
+    vals = (dt(1.5) * n3) / np.where(zero, dt(1), d)
+    return np.where(zero, dt(0), vals).astype(V.dtype), zero
+
+
 def run_2way(V):
     """(values, degenerate mask, checksum hex) of a full single-rank 2-way run."""
     vals, zero = values_2way(V)

@@ -79,6 +79,9 @@ SIGNATURES = {
     "psim_fold_add": (C.c_int, [C.c_int, c_vp, c_vp, c_i64, c_vp]),
     "psim_box3_plan": (C.c_int, [C.c_int, C.POINTER(Box3), C.POINTER(c_i64), C.POINTER(c_i64)]),
     "psim_czek3_box": (C.c_int, [C.c_int, C.POINTER(Box3), c_vp]),
+    "psim_czek3_box_numerators": (C.c_int, [C.c_int, C.POINTER(Box3), c_vp]),
+    "psim_czek3_from_numerators": (
+        C.c_int, [C.c_int, C.POINTER(Box3), c_vp, c_i64, c_i64, c_vp, c_vp]),
     "psim_peak_minplus": (
         C.c_int, [C.c_int, C.c_int, c_i64, C.POINTER(C.c_double), C.POINTER(C.c_double), c_vp]),
 }

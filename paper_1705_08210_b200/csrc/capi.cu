@@ -206,18 +206,23 @@ int psim_box3_plan(int dtype, const psim_box3_t* box, int64_t* n_out, int64_t* n
   return PSIM_OK;
 }
 
-int psim_czek3_box(int dtype, const psim_box3_t* b, void* stream) {
+static int check_box(int dtype, const psim_box3_t* b, bool tables) {
   if (int r = check_dtype(dtype)) return r;
   if (!b) return fail(PSIM_ECONFIG, "box is NULL");
   if (b->n_f < 0) return fail(PSIM_ECONFIG, "negative n_f");
   if (int r = check_operand(dtype, b->VA, b->ldA, b->n_f, "VA")) return r;
   if (int r = check_operand(dtype, b->VB, b->ldB, b->n_f, "VB")) return r;
   if (int r = check_operand(dtype, b->VC, b->ldC, b->n_f, "VC")) return r;
-  if (!b->SA || !b->SB || !b->SC || !b->NAB || !b->NAC || !b->NBC || !b->acc)
+  if (tables && (!b->SA || !b->SB || !b->SC || !b->NAB || !b->NAC || !b->NBC || !b->acc))
     return fail(PSIM_ECONFIG, "NULL sums / numerator table / acc");
   if (b->i0 < b->a0 || b->j0 < b->b0 || b->k0 < b->c0 || b->i1 > b->n_v || b->j1 > b->n_v ||
       b->k1 > b->n_v)
     return fail(PSIM_ECONFIG, "box intervals outside their blocks");
+  return PSIM_OK;
+}
+
+// mode 0: fused values (psim_czek3_box); 1: raw n_ijk (psim_czek3_box_numerators)
+static int run_box(int dtype, const psim_box3_t* b, int mode, void* stream, const char* what) {
   std::vector<int64_t> tp, op;
   box3_counts(dtype, *b, &tp, &op);
   const int64_t n_tiles = tp.back();
@@ -225,11 +230,43 @@ int psim_czek3_box(int dtype, const psim_box3_t* b, void* stream) {
   cudaStream_t st = S(stream);
   int64_t* d = nullptr;
   cudaError_t e = cudaMallocAsync(&d, 2 * tp.size() * sizeof(int64_t), st);
-  if (e != cudaSuccess) return cuda_status(e, "psim_czek3_box workspace");
-  e = psim::czek3_box(dtype, *b, d, n_tiles, st);
+  if (e != cudaSuccess) return cuda_status(e, what);
+  e = mode ? psim::czek3_box_numerators(dtype, *b, d, n_tiles, st)
+           : psim::czek3_box(dtype, *b, d, n_tiles, st);
   cudaError_t e2 = cudaFreeAsync(d, st);
   if (e == cudaSuccess) e = e2;
-  return cuda_status(e, "psim_czek3_box");
+  return cuda_status(e, what);
+}
+
+int psim_czek3_box(int dtype, const psim_box3_t* b, void* stream) {
+  if (int r = check_box(dtype, b, true)) return r;
+  return run_box(dtype, b, 0, stream, "psim_czek3_box");
+}
+
+int psim_czek3_box_numerators(int dtype, const psim_box3_t* b, void* stream) {
+  if (int r = check_box(dtype, b, false)) return r;
+  if (!b->vals) return fail(PSIM_ECONFIG, "vals (the n_ijk output) is NULL");
+  return run_box(dtype, b, 1, stream, "psim_czek3_box_numerators");
+}
+
+int psim_czek3_from_numerators(int dtype, const psim_box3_t* b, const void* n3, int64_t e0,
+                               int64_t e1, void* vals, void* stream) {
+  if (int r = check_dtype(dtype)) return r;
+  if (!b || !n3) return fail(PSIM_ECONFIG, "NULL box / numerators");
+  if (!b->SA || !b->SB || !b->SC || !b->NAB || !b->NAC || !b->NBC || !b->acc)
+    return fail(PSIM_ECONFIG, "NULL sums / numerator table / acc");
+  std::vector<int64_t> tp, op;
+  box3_counts(dtype, *b, &tp, &op);
+  if (e0 < 0 || e1 > op.back() || e0 > e1) return fail(PSIM_ECONFIG, "element range outside box");
+  if (e1 == e0) return PSIM_OK;
+  cudaStream_t st = S(stream);
+  int64_t* d = nullptr;
+  cudaError_t e = cudaMallocAsync(&d, 2 * tp.size() * sizeof(int64_t), st);
+  if (e != cudaSuccess) return cuda_status(e, "psim_czek3_from_numerators workspace");
+  e = psim::czek3_from_num(dtype, *b, d, n3, e0, e1, vals, st);
+  cudaError_t e2 = cudaFreeAsync(d, st);
+  if (e == cudaSuccess) e = e2;
+  return cuda_status(e, "psim_czek3_from_numerators");
 }
 
 int psim_peak_minplus(int dtype, int variant, int64_t iters, double* cmp_per_s,

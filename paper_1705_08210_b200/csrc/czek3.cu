@@ -27,7 +27,25 @@
 
 namespace psim {
 
-template <class C>
+// Eq. 1 for one triple (metrics3.py:38-44 with canonical roles i<j<k,
+// metrics3.py:146, 175-182): local columns ai (block A), jb (B), kc (C).
+template <typename T>
+__device__ __forceinline__ T czek3_value(const Czek3Box& b, int64_t ai, int64_t jb, int64_t kc,
+                                         T n_ijk, bool& zero) {
+  const T* SA = static_cast<const T*>(b.SA);
+  const T* SB = static_cast<const T*>(b.SB);
+  const T* SC = static_cast<const T*>(b.SC);
+  const T nij = static_cast<const T*>(b.NAB)[ai + jb * b.ldAB];
+  const T nik = static_cast<const T*>(b.NAC)[ai + kc * b.ldAC];
+  const T njk = static_cast<const T*>(b.NBC)[jb + kc * b.ldBC];
+  const T d = Traits<T>::add(Traits<T>::add(SA[ai], SB[jb]), SC[kc]);
+  const T n3 = Traits<T>::sub(Traits<T>::add(Traits<T>::add(nij, nik), njk), n_ijk);
+  zero = (d == T(0));
+  return zero ? T(0) : Traits<T>::div(Traits<T>::mul(T(1.5), n3), d);
+}
+
+// RAW = true writes the n_ijk partial sums (field-split path) instead of values.
+template <class C, bool RAW>
 __global__ void __launch_bounds__(kNT, C::MINB)
     k_czek3(const Czek3Box b, const int64_t* __restrict__ tile_pref,
             const int64_t* __restrict__ out_pref, int64_t nJ) {
@@ -64,18 +82,25 @@ __global__ void __launch_bounds__(kNT, C::MINB)
   minplus_tile<C, true>(VA + ia * b.ldA, b.ldA, rows, VC + kc * b.ldC, b.ldC, cols,
                         VB + jb * b.ldB, b.n_f, acc, smem);
 
-  const T* SA = static_cast<const T*>(b.SA);
-  const T* SB = static_cast<const T*>(b.SB);
-  const T* SC = static_cast<const T*>(b.SC);
-  const T* NAB = static_cast<const T*>(b.NAB);
-  const T* NAC = static_cast<const T*>(b.NAC);
-  const T* NBC = static_cast<const T*>(b.NBC);
   T* out = static_cast<T*>(b.vals);
-  const T sj = SB[jb];
   const int64_t obase = out_pref[lo];
   const uint64_t nv = (uint64_t)b.n_v;
 
   const int ty = thread_ty(), tx = thread_tx();
+  if (RAW) {
+#pragma unroll
+    for (int mi = 0; mi < C::TM; ++mi) {
+      const int li = ty + 16 * mi;
+      if (li >= rows) continue;
+      const int64_t orow = obase + (r0 + li) * ncols + c0;
+#pragma unroll
+      for (int nk = 0; nk < C::TN; ++nk) {
+        const int lk = tx + 16 * nk;
+        if (lk < cols) out[orow + lk] = acc[mi][nk];
+      }
+    }
+    return;
+  }
   Cks c;
 #pragma unroll
   for (int mi = 0; mi < C::TM; ++mi) {
@@ -83,9 +108,6 @@ __global__ void __launch_bounds__(kNT, C::MINB)
     if (li >= rows) continue;
     const int64_t ai = ia + li;            // local in A
     const int64_t i = b.a0 + ai;           // global
-    const T si = SA[ai];
-    const T nij = NAB[ai + jb * b.ldAB];
-    const T sij = Traits<T>::add(si, sj);
     // triple_index(i, j, k) = base_ij + (k - j - 1), base_ij = C3(n)-C3(n-i)+pair_index(j-i-1, j-i, n-i-1)
     const uint64_t base_ij = choose3(nv) - choose3(nv - (uint64_t)i) +
                              pair_index((uint64_t)(j - i - 1), (uint64_t)(j - i), nv - (uint64_t)i - 1);
@@ -96,18 +118,46 @@ __global__ void __launch_bounds__(kNT, C::MINB)
       if (lk >= cols) continue;
       const int64_t kcl = kc + lk;          // local in C
       const int64_t k = b.c0 + kcl;         // global
-      const T nik = NAC[ai + kcl * b.ldAC];
-      const T njk = NBC[jb + kcl * b.ldBC];
-      const T d = Traits<T>::add(sij, SC[kcl]);
-      const T n3 = Traits<T>::sub(Traits<T>::add(Traits<T>::add(nij, nik), njk), acc[mi][nk]);
-      const bool zero = (d == T(0));
-      const T v = zero ? T(0) : Traits<T>::div(Traits<T>::mul(T(1.5), n3), d);
+      bool zero;
+      const T v = czek3_value<T>(b, ai, jb, kcl, acc[mi][nk], zero);
       if (out) out[orow + lk] = v;
       c.term(base_ij + (uint64_t)(k - j - 1), Traits<T>::bits(v));
       c.deg += zero ? 1ull : 0ull;
     }
   }
   cks_block_flush<kNT>(b.acc, c);
+}
+
+// Values + checksum for elements [e0, e1) of a box's pivot-major layout from
+// already-folded n_ijk sums (the 3-way field-split path: partial n_ijk ->
+// ordered fold over p_f -> this epilogue; metrics3.py:163-182). N3 and vals
+// point at element e0. out_pref: the box's per-pivot output prefix (device).
+template <typename T>
+__global__ void __launch_bounds__(256) k_czek3_from_num(const Czek3Box b,
+                                                        const int64_t* __restrict__ out_pref,
+                                                        int64_t nJ, const T* __restrict__ N3,
+                                                        int64_t e0, int64_t e1, T* __restrict__ vals) {
+  Cks c;
+  const uint64_t nv = (uint64_t)b.n_v;
+  for (int64_t e = e0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < e1;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = nJ;  // largest lo with out_pref[lo] <= e
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (out_pref[mid] <= e) lo = mid; else hi = mid;
+    }
+    const int64_t j = b.j0 + lo;
+    const int64_t klo = max64(b.k0, j + 1);
+    const int64_t ncols = b.k1 - klo;
+    const int64_t off = e - out_pref[lo];
+    const int64_t i = b.i0 + off / ncols, k = klo + off % ncols;
+    bool zero;
+    const T v = czek3_value<T>(b, i - b.a0, j - b.b0, k - b.c0, N3[e - e0], zero);
+    if (vals) vals[e - e0] = v;
+    c.term(triple_index((uint64_t)i, (uint64_t)j, (uint64_t)k, nv), Traits<T>::bits(v));
+    c.deg += zero ? 1ull : 0ull;
+  }
+  cks_block_flush<256>(b.acc, c);
 }
 
 // Per-pivot prefix sums of CTA tiles and output elements for a box, one CTA:
@@ -161,11 +211,11 @@ __global__ void __launch_bounds__(1024) k_box3_prefix(int64_t i0, int64_t i1, in
   }
 }
 
-template <typename T>
+template <typename T, bool RAW>
 static cudaError_t czek3_t(const Czek3Box& b, int64_t* work, int64_t n_tiles, cudaStream_t st) {
   using C = typename Prod<T>::C;
-  cudaError_t e = cudaFuncSetAttribute(k_czek3<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       C::SMEM_BYTES);
+  cudaError_t e = cudaFuncSetAttribute(k_czek3<C, RAW>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
   if (e != cudaSuccess) return e;
   if (n_tiles <= 0) return cudaSuccess;
   if (n_tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
@@ -173,8 +223,36 @@ static cudaError_t czek3_t(const Czek3Box& b, int64_t* work, int64_t n_tiles, cu
   int64_t* tp = work;
   int64_t* op = work + nJ + 1;
   k_box3_prefix<<<1, 1024, 0, st>>>(b.i0, b.i1, b.j0, b.j1, b.k0, b.k1, C::BM, C::BN, tp, op);
-  k_czek3<C><<<(unsigned)n_tiles, kNT, C::SMEM_BYTES, st>>>(b, tp, op, nJ);
+  k_czek3<C, RAW><<<(unsigned)n_tiles, kNT, C::SMEM_BYTES, st>>>(b, tp, op, nJ);
   return cudaGetLastError();
+}
+
+template <typename T>
+static cudaError_t czek3_from_num_t(const Czek3Box& b, int64_t* work, const void* n3, int64_t e0,
+                                    int64_t e1, void* vals, cudaStream_t st) {
+  using C = typename Prod<T>::C;
+  if (e1 <= e0) return cudaSuccess;
+  const int64_t nJ = b.j1 - b.j0;
+  int64_t* tp = work;
+  int64_t* op = work + nJ + 1;
+  k_box3_prefix<<<1, 1024, 0, st>>>(b.i0, b.i1, b.j0, b.j1, b.k0, b.k1, C::BM, C::BN, tp, op);
+  int64_t blocks = (e1 - e0 + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  k_czek3_from_num<T><<<(unsigned)blocks, 256, 0, st>>>(b, op, nJ, static_cast<const T*>(n3), e0,
+                                                        e1, static_cast<T*>(vals));
+  return cudaGetLastError();
+}
+
+cudaError_t czek3_box_numerators(int dtype, const Czek3Box& b, int64_t* d_work, int64_t n_tiles,
+                                 cudaStream_t st) {
+  return dtype == kF64 ? czek3_t<double, true>(b, d_work, n_tiles, st)
+                       : czek3_t<float, true>(b, d_work, n_tiles, st);
+}
+
+cudaError_t czek3_from_num(int dtype, const Czek3Box& b, int64_t* d_work, const void* n3,
+                           int64_t e0, int64_t e1, void* vals, cudaStream_t st) {
+  return dtype == kF64 ? czek3_from_num_t<double>(b, d_work, n3, e0, e1, vals, st)
+                       : czek3_from_num_t<float>(b, d_work, n3, e0, e1, vals, st);
 }
 
 void tile_shape(int dtype, int* bm, int* bn) {
@@ -189,8 +267,8 @@ void tile_shape(int dtype, int* bm, int* bn) {
 
 cudaError_t czek3_box(int dtype, const Czek3Box& b, int64_t* d_work, int64_t n_tiles,
                       cudaStream_t st) {
-  return dtype == kF64 ? czek3_t<double>(b, d_work, n_tiles, st)
-                       : czek3_t<float>(b, d_work, n_tiles, st);
+  return dtype == kF64 ? czek3_t<double, false>(b, d_work, n_tiles, st)
+                       : czek3_t<float, false>(b, d_work, n_tiles, st);
 }
 
 }  // namespace psim

@@ -46,6 +46,12 @@ cudaError_t czek2_from_num(int dtype, const void* N, int64_t r0, int64_t r1, int
 // on the device in `d_work` (2 * (j1 - j0 + 1) int64).
 cudaError_t czek3_box(int dtype, const Czek3Box& b, int64_t* d_work, int64_t n_tiles,
                       cudaStream_t st);
+// Same box, writing the n_ijk partial sums to b.vals instead of values.
+cudaError_t czek3_box_numerators(int dtype, const Czek3Box& b, int64_t* d_work, int64_t n_tiles,
+                                 cudaStream_t st);
+// Values + checksum of elements [e0, e1) of the box from folded n_ijk.
+cudaError_t czek3_from_num(int dtype, const Czek3Box& b, int64_t* d_work, const void* n3,
+                           int64_t e0, int64_t e1, void* vals, cudaStream_t st);
 
 cudaError_t peak_minplus(int dtype, int variant, int64_t iters, double* cmp_per_s,
                          double* cmp_per_clk_sm, cudaStream_t st);

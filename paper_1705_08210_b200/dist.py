@@ -96,7 +96,8 @@ def piece_count(pc) -> int:
                 - packed_offset(pc.r0, pc.m, pc.n, pc.diagonal))
     from .plan import Box, box_count
 
-    return box_count(Box((0, 0, 0), pc.i0, pc.i1, pc.j0, pc.j1, pc.k0, pc.k1))
+    full = box_count(Box((0, 0, 0), pc.i0, pc.i1, pc.j0, pc.j1, pc.k0, pc.k1))
+    return (full if pc.e1 is None else pc.e1) - pc.e0
 
 
 def gather_totals(acc: torch.Tensor, count: int, world: int, dev) -> tuple[int, int, int, int]:
@@ -136,6 +137,24 @@ def reduce_scatter_rows(part: torch.Tensor, m: int, n: int, diagonal: bool, p_f:
         fold(total, recv[f * mine:(f + 1) * mine])
     r0, r1 = chunks[p_f]
     return total, r0, r1
+
+
+def reduce_scatter_flat(part: torch.Tensor, p_f: int, n_pf: int, group,
+                        fold) -> tuple[torch.Tensor, int, int]:
+    """Ordered field-axis reduction of a flat partial array (3-way boxes):
+    element range f of n_pf equal ranges goes to field rank f, folded in
+    ascending p_f. Returns (folded chunk, e0, e1)."""
+    count = part.numel()
+    bounds = [count * f // n_pf for f in range(n_pf + 1)]
+    sizes = [bounds[f + 1] - bounds[f] for f in range(n_pf)]
+    mine = sizes[p_f]
+    recv = torch.empty(mine * n_pf, dtype=part.dtype, device=part.device)
+    dist.all_to_all_single(recv, part, output_split_sizes=[mine] * n_pf,
+                           input_split_sizes=sizes, group=group)
+    total = recv[:mine].clone()
+    for f in range(1, n_pf):
+        fold(total, recv[f * mine:(f + 1) * mine])
+    return total, bounds[p_f], bounds[p_f + 1]
 
 
 def fold_over_field(local_parts: torch.Tensor, code: int, group, n_pf: int) -> torch.Tensor:

@@ -24,20 +24,25 @@ from .records import BoxPiece
 
 def box_struct(box: Box, blocks: dict, sums: dict, tables, n_f: int, n_v: int,
                vals, acc) -> N.Box3:
+    """psim_box3_t for `box`; tables / sums may be None (raw-numerator launches)."""
     A, B, Cb = box.blocks
     bA, bB, bC = blocks[A], blocks[B], blocks[Cb]
-    NAB, NAC, NBC = tables(A, B), tables(A, Cb), tables(B, Cb)
-    return N.Box3(
+    b = N.Box3(
         n_f=n_f, n_v=n_v,
         VA=D.ptr(bA.data), ldA=bA.ld, a0=bA.v0,
         VB=D.ptr(bB.data), ldB=bB.ld, b0=bB.v0,
         VC=D.ptr(bC.data), ldC=bC.ld, c0=bC.v0,
-        SA=D.ptr(sums[A]), SB=D.ptr(sums[B]), SC=D.ptr(sums[Cb]),
-        NAB=D.ptr(NAB), ldAB=NAB.shape[1], NAC=D.ptr(NAC), ldAC=NAC.shape[1],
-        NBC=D.ptr(NBC), ldBC=NBC.shape[1],
         i0=box.i0, i1=box.i1, j0=box.j0, j1=box.j1, k0=box.k0, k1=box.k1,
         vals=D.ptr(vals), acc=D.ptr(acc),
     )
+    if sums is not None:
+        b.SA, b.SB, b.SC = D.ptr(sums[A]), D.ptr(sums[B]), D.ptr(sums[Cb])
+    if tables is not None:
+        NAB, NAC, NBC = tables(A, B), tables(A, Cb), tables(B, Cb)
+        b.NAB, b.ldAB = D.ptr(NAB), NAB.shape[1]
+        b.NAC, b.ldAC = D.ptr(NAC), NAC.shape[1]
+        b.NBC, b.ldBC = D.ptr(NBC), NBC.shape[1]
+    return b
 
 
 def box_plan(b: N.Box3, code: int = N.F64) -> tuple[int, int]:
@@ -62,6 +67,73 @@ class Tables:
         return self.cache[key]
 
 
+class FieldFoldedTables:
+    """NCCL field split: this rank's slab table, all-gathered over the field
+    group and folded in ascending p_f (every field rank computes the same
+    folded table; all field ranks request tables in the same order)."""
+
+    def __init__(self, blocks: dict, code: int, group, n_pf: int):
+        self.local = Tables(blocks, code)
+        self.code, self.group, self.n_pf = code, group, n_pf
+        self.cache: dict = {}
+
+    def __call__(self, X: int, Y: int) -> torch.Tensor:
+        if (X, Y) not in self.cache:
+            from .dist import fold_over_field
+
+            part = self.local(X, Y)
+            self.cache[X, Y] = fold_over_field(part, self.code, self.group, self.n_pf)
+            del self.local.cache[X, Y]
+        return self.cache[X, Y]
+
+
+class FoldedTables:
+    """Numerator tables over a field split: each field slab's table, folded in
+    ascending p_f order (the reference reduces P_bc and the per-pivot
+    column sums the same way, metrics3.py:149, 163-164; engine.py:197-216)."""
+
+    def __init__(self, slab_tables: list, code: int):
+        self.slab_tables, self.code, self.cache = slab_tables, code, {}
+
+    def __call__(self, X: int, Y: int) -> torch.Tensor:
+        if (X, Y) not in self.cache:
+            total = self.slab_tables[0](X, Y).clone()
+            for t in self.slab_tables[1:]:
+                D.fold_(total, t(X, Y), self.code)
+            self.cache[X, Y] = total
+        return self.cache[X, Y]
+
+
+def run_boxes_field(code, problem, boxes, slab_blocks, sums, tables, acc, keep_values,
+                    pieces) -> int:
+    """Boxes over a field split on one device: per-slab raw n_ijk, ordered fold,
+    then the epilogue from folded numerators."""
+    count = 0
+    tdt = D.torch_dtype(problem.precision)
+    dev = acc.device
+    for box in boxes:
+        n_out, _ = box_plan(box_struct(box, slab_blocks[0], None, None, problem.n_f, problem.n_v,
+                                       None, acc), code)
+        if n_out == 0:
+            continue
+        total = torch.empty(n_out, dtype=tdt, device=dev)
+        part = torch.empty_like(total) if len(slab_blocks) > 1 else None
+        for f, blocks in enumerate(slab_blocks):
+            dst = total if f == 0 else part
+            b = box_struct(box, blocks, None, None, blocks[box.blocks[0]].n_fp, problem.n_v, dst,
+                           acc)
+            N.call("psim_czek3_box_numerators", code, C.byref(b), D.stream_ptr())
+            if f:
+                D.fold_(total, part, code)
+        vals = torch.empty(n_out, dtype=tdt, device=dev) if keep_values else None
+        b = box_struct(box, slab_blocks[0], sums, tables, problem.n_f, problem.n_v, None, acc)
+        N.call("psim_czek3_from_numerators", code, C.byref(b), D.ptr(total), 0, n_out,
+               D.ptr(vals), D.stream_ptr())
+        pieces.append(BoxPiece(box.i0, box.i1, box.j0, box.j1, box.k0, box.k1, vals))
+        count += n_out
+    return count
+
+
 def run_boxes(code, problem, boxes, blocks, sums, tables, acc, keep_values, pieces) -> int:
     count = 0
     tdt = D.torch_dtype(problem.precision)
@@ -80,16 +152,20 @@ def run_boxes(code, problem, boxes, blocks, sums, tables, acc, keep_values, piec
 
 
 def run_local(problem, grid, stages, keep_values: bool = True) -> Outcome:
-    if grid.n_pf != 1:
-        raise ConfigError("3-way runs with a field-axis split (n_pf > 1) are not supported yet")
     dev = torch.device("cuda", torch.cuda.current_device())
     code = D.code_of(problem.precision)
     n_vp = problem.n_v // grid.n_pv
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record()
-    blocks = {p: D.load_block(problem, grid, RankCoords(0, p, 0), dev) for p in range(grid.n_pv)}
-    sums = {p: fold_sums([D.column_sums(blocks[p])], code) for p in range(grid.n_pv)}
-    tables = Tables(blocks, code)
+    slab_blocks = [{p: D.load_block(problem, grid, RankCoords(f, p, 0), dev)
+                    for p in range(grid.n_pv)} for f in range(grid.n_pf)]
+    blocks = slab_blocks[0]
+    sums = {p: fold_sums([D.column_sums(sb[p]) for sb in slab_blocks], code)
+            for p in range(grid.n_pv)}
+    if grid.n_pf == 1:
+        tables = Tables(blocks, code)
+    else:
+        tables = FoldedTables([Tables(sb, code) for sb in slab_blocks], code)
     acc = D.new_acc(dev)
     pieces: list = []
     count = 0
@@ -99,8 +175,12 @@ def run_local(problem, grid, stages, keep_values: bool = True) -> Outcome:
             for ev in plan_3way(grid, RankCoords(0, p_v, p_r)):
                 if isinstance(ev, Unit3):
                     boxes.extend(unit_boxes(ev, n_vp, grid.n_st, stages))
-            count += run_boxes(code, problem, merge_boxes(boxes), blocks, sums, tables, acc,
-                               keep_values, pieces)
+            if grid.n_pf == 1:
+                count += run_boxes(code, problem, merge_boxes(boxes), blocks, sums, tables, acc,
+                                   keep_values, pieces)
+            else:
+                count += run_boxes_field(code, problem, merge_boxes(boxes), slab_blocks, sums,
+                                         tables, acc, keep_values, pieces)
     end.record()
     end.synchronize()
     lo, hi, deg = D.acc_words(acc)
@@ -123,16 +203,15 @@ class Runner3Dist:
 
     def __init__(self, problem, grid, stages, keep_values: bool = True,
                  out_budget: float | None = None):
-        from .dist import ensure_initialized
+        from .dist import ensure_initialized, field_group
 
-        if grid.n_pf != 1:
-            raise ConfigError("3-way runs with a field-axis split (n_pf > 1) are not supported yet")
         self.world, self.rank = ensure_initialized(grid)
         from .domain import coords_of_rank
 
         self.problem, self.grid, self.stages = problem, grid, tuple(stages)
         self.keep, self.out_budget = keep_values, out_budget
         self.coords = coords_of_rank(self.rank, grid)
+        self.group = field_group(grid, self.coords)
         self.code = D.code_of(problem.precision)
         self.n_vp = problem.n_v // grid.n_pv
         units = [e for e in plan_3way(grid, self.coords) if isinstance(e, Unit3)]
@@ -169,10 +248,13 @@ class Runner3Dist:
                                         slab * self.n_vp, p.precision)
         self.sums = {s: torch.empty(self.n_vp, dtype=own.data.dtype, device=dev)
                      for s in self.blocks}
-        self.tables = Tables(self.blocks, self.code)
+        if g.n_pf == 1:
+            self.tables = Tables(self.blocks, self.code)
+        else:
+            self.tables = FieldFoldedTables(self.blocks, self.code, self.group, g.n_pf)
         self.acc = D.new_acc(dev)
         self.buf = None
-        if self.out_budget is not None:
+        if self.out_budget is not None and g.n_pf == 1:
             sizes = [box_plan(self._struct(b, None))[0] for b in self.edge_boxes + self.rest_boxes]
             self.buf = torch.empty(max(sizes + [1]), dtype=D.torch_dtype(p.precision), device=dev)
 
@@ -180,7 +262,35 @@ class Runner3Dist:
         p = self.problem
         return box_struct(box, self.blocks, self.sums, self.tables, p.n_f, p.n_v, vals, self.acc)
 
+    def _run_field(self, boxes):
+        """Field split: raw n_ijk of this slab -> ordered reduce-scatter over the
+        field group -> values for this rank's element share."""
+        from .dist import reduce_scatter_flat
+
+        p, g = self.problem, self.grid
+        tdt = D.torch_dtype(p.precision)
+        for box in boxes:
+            n_out, _ = box_plan(self._struct(box, None))
+            if n_out == 0:
+                continue
+            part = torch.empty(n_out, dtype=tdt, device=self.dev)
+            raw = box_struct(box, self.blocks, None, None, self.blocks[box.blocks[0]].n_fp, p.n_v,
+                             part, self.acc)
+            N.call("psim_czek3_box_numerators", self.code, C.byref(raw), D.stream_ptr())
+            total, e0, e1 = reduce_scatter_flat(part, self.coords.p_f, g.n_pf, self.group,
+                                                lambda d, s: D.fold_(d, s, self.code))
+            vals = torch.empty(e1 - e0, dtype=tdt, device=self.dev) if self.keep else None
+            b = self._struct(box, None)
+            if e1 > e0:
+                N.call("psim_czek3_from_numerators", self.code, C.byref(b), D.ptr(total), e0, e1,
+                       D.ptr(vals), D.stream_ptr())
+            self.pieces.append(BoxPiece(box.i0, box.i1, box.j0, box.j1, box.k0, box.k1, vals,
+                                        e0, e1))
+            self.count += e1 - e0
+
     def _run(self, boxes, timed, events):
+        if self.grid.n_pf > 1:
+            return self._run_field(boxes)
         tdt = D.torch_dtype(self.problem.precision)
         for box in boxes:
             n_out, _ = box_plan(self._struct(box, None))
@@ -209,7 +319,12 @@ class Runner3Dist:
         self.acc.zero_()
         self.pieces, self.count = [], 0
         own = self.blocks[me]
-        self.sums[me].copy_(D.column_sums(own))
+        s = D.column_sums(own)
+        if g.n_pf > 1:
+            from .dist import fold_over_field
+
+            s = fold_over_field(s, self.code, self.group, g.n_pf)
+        self.sums[me].copy_(s)
         self.tables.cache.clear()
         works = []
         if g.n_pv > 1:

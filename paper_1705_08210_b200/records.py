@@ -63,6 +63,8 @@ class BoxPiece:
     k0: int
     k1: int
     values: object
+    e0: int = 0            # element sub-range held (field-split share)
+    e1: int | None = None
 
     def canonical(self, n_v: int) -> np.ndarray:
         parts = []
@@ -73,7 +75,8 @@ class BoxPiece:
             i = np.repeat(np.arange(self.i0, ihi, dtype=np.int64), self.k1 - klo)
             k = np.tile(np.arange(klo, self.k1, dtype=np.int64), ihi - self.i0)
             parts.append(triple_index_np(i, np.full_like(i, j), k, n_v))
-        return np.concatenate(parts) if parts else np.zeros(0, np.int64)
+        idx = np.concatenate(parts) if parts else np.zeros(0, np.int64)
+        return idx[self.e0:self.e1]
 
 
 def _to_numpy(t) -> np.ndarray:

@@ -129,6 +129,11 @@ def main():
     cases.append(run_case("uniform", 2, "double", 1000, 120, DecompGrid(n_pf=8), 17, values=True))
     cases.append(run_case("uniform", 2, "single", 1000, 120, DecompGrid(n_pf=4, n_pv=2), 17,
                           values=True))
+    cases.append(run_case("uniform", 3, "double", 200, 24, DecompGrid(n_pf=2), 23, values=True))
+    cases.append(run_case("uniform", 3, "single", 300, 24, DecompGrid(n_pf=4, n_pv=2), 29,
+                          values=True))
+    cases.append(run_case("random-exact", 3, "double", 64, 24, DecompGrid(n_pf=2, n_pr=2), 402,
+                          11))
     # edge cases from the reference tests
     m2 = np.zeros((4, 4))
     m2[:, 0] = [1, 2, 0, 1]

@@ -60,8 +60,6 @@ CASES = golden()["cases"]
 @pytest.mark.parametrize("idx", range(len(CASES)))
 def test_golden_case(idx):
     case = CASES[idx]
-    if case["arity"] == 3 and case["grid"]["n_pf"] > 1:
-        pytest.skip("3-way field split not implemented yet")
     res = _run(case, case.get("stage"))
     assert len(res.records) == case["records"]
     assert res.checksum.hex == case["checksum"]

@@ -42,10 +42,12 @@ def main():
         (2, "double", 777, 120, dict(n_pr=world)),
         (3, "double", 300, 12 * world, dict(n_pv=world)),
         (3, "single", 200, 24, dict(n_pr=world)),
+        (3, "double", 200, 24, dict(n_pf=world)),
     ]
     if world % 2 == 0:
         extra.append((2, "double", 500, 96, dict(n_pf=2, n_pv=world // 2)))
         extra.append((3, "double", 64, 24, dict(n_pv=2, n_pr=world // 2)))
+        extra.append((3, "single", 300, 24, dict(n_pf=2, n_pv=world // 2)))
     for arity, prec, n_f, n_v, g in extra:
         cases.append((dict(kind="uniform", arity=arity, precision=prec, n_f=n_f, n_v=n_v, seed=31,
                            grid=dict(dict(n_pf=1, n_pv=1, n_pr=1, n_st=1), **g)), "local"))
