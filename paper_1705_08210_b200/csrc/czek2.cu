@@ -35,7 +35,8 @@ struct Args2 {
   int64_t tiles_m, tiles_n;   // tile grid of this launch
   int64_t row_tile0;          // first row-tile of the launch (row band)
   int64_t m_end;              // rows >= m_end are outside the band
-  const int64_t* row_pref;    // diagonal tasks: tiles before each row-tile (device)
+  int64_t band, nbands;       // rasterisation: row-tiles per band, bands in the launch
+  const int64_t* row_pref;    // tiles before each band (device), see band_tile
 };
 
 // Position of local pair (i, j) in the packed layout shared by values and
@@ -52,12 +53,9 @@ __global__ void __launch_bounds__(kNT, C::MINB) k_minplus2(const Args2<typename 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* smem = reinterpret_cast<T*>(smem_raw);
   int bi, bj;
-  if (a.diagonal) {
-    diag_tile((int64_t)blockIdx.x, a.row_pref, a.tiles_m, a.row_tile0, C::BM, C::BN, bi, bj);
-  } else {
-    bi = (int)(a.row_tile0 + blockIdx.x / a.tiles_n);
-    bj = (int)(blockIdx.x % a.tiles_n);
-  }
+  if (!band_tile((int64_t)blockIdx.x, a.row_pref, a.nbands, a.band, a.row_tile0,
+                 a.row_tile0 + a.tiles_m, C::BM, C::BN, a.diagonal, bi, bj))
+    return;  // left of the diagonal inside a diagonal band (uniform per CTA)
   const int64_t row0 = (int64_t)bi * C::BM, col0 = (int64_t)bj * C::BN;
   const int rows = (int)min64(C::BM, a.m_end - row0);
   const int cols = (int)min64(C::BN, a.n - col0);
@@ -116,19 +114,27 @@ __global__ void __launch_bounds__(kNT, C::MINB) k_minplus2(const Args2<typename 
   }
 }
 
-// Row-tile prefix of a diagonal task's tile grid (see diag_tile): one CTA,
-// each thread folds a contiguous range of row-tiles, then a block scan.
-__global__ void __launch_bounds__(1024) k_diag_prefix(int64_t tiles_m, int64_t row_tile0,
+// Tiles (CTAs) of band b of a launch (see band_tile).
+__host__ __device__ __forceinline__ int64_t band_count(int64_t b, int64_t G, int64_t row_tile0,
+                                                       int64_t tiles_m, int64_t tiles_n,
+                                                       int64_t bm, int64_t bn, int diagonal) {
+  const int64_t r0 = row_tile0 + b * G;
+  const int64_t rows = min64(G, row_tile0 + tiles_m - r0);
+  return rows * max64(0, tiles_n - first_col_tile(r0, bm, bn, diagonal));
+}
+
+// Band prefix of a launch's tile grid: one CTA, each thread folds a
+// contiguous range of bands, then a block scan.
+__global__ void __launch_bounds__(1024) k_band_prefix(int64_t nbands, int64_t G,
+                                                      int64_t row_tile0, int64_t tiles_m,
                                                       int64_t tiles_n, int64_t bm, int64_t bn,
-                                                      int64_t* __restrict__ pref) {
+                                                      int diagonal, int64_t* __restrict__ pref) {
   __shared__ int64_t s[1024];
-  const int64_t per = (tiles_m + blockDim.x - 1) / blockDim.x;
-  const int64_t a = min64(tiles_m, threadIdx.x * per), e = min64(tiles_m, a + per);
-  auto count = [&](int64_t b) {
-    return max64(0, tiles_n - ((row_tile0 + b) * bm + 1) / bn);
-  };
+  const int64_t per = (nbands + blockDim.x - 1) / blockDim.x;
+  const int64_t a = min64(nbands, threadIdx.x * per), e = min64(nbands, a + per);
   int64_t sum = 0;
-  for (int64_t b = a; b < e; ++b) sum += count(b);
+  for (int64_t b = a; b < e; ++b)
+    sum += band_count(b, G, row_tile0, tiles_m, tiles_n, bm, bn, diagonal);
   s[threadIdx.x] = sum;
   __syncthreads();
   for (int off = 1; off < (int)blockDim.x; off <<= 1) {
@@ -140,19 +146,21 @@ __global__ void __launch_bounds__(1024) k_diag_prefix(int64_t tiles_m, int64_t r
   int64_t run = threadIdx.x ? s[threadIdx.x - 1] : 0;
   for (int64_t b = a; b < e; ++b) {
     pref[b] = run;
-    run += count(b);
+    run += band_count(b, G, row_tile0, tiles_m, tiles_n, bm, bn, diagonal);
   }
-  if (threadIdx.x == blockDim.x - 1) pref[tiles_m] = s[threadIdx.x];
+  if (threadIdx.x == blockDim.x - 1) pref[nbands] = s[threadIdx.x];
 }
 
+// Band height: about sqrt(resident CTAs) row-tiles, so the resident window
+// is roughly square in tiles (fewest distinct panels in flight).
 template <class C>
-static int64_t diag_tiles(int64_t tiles_m, int64_t row_tile0, int64_t tiles_n) {
-  int64_t t = 0;
-  for (int64_t b = row_tile0; b < row_tile0 + tiles_m; ++b) {
-    const int64_t c = tiles_n - (b * C::BM + 1) / C::BN;
-    t += c > 0 ? c : 0;
-  }
-  return t;
+static int64_t band_height() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const double resident = (double)sms * C::MINB;
+  int64_t g = (int64_t)(sqrt(resident * C::BN / (double)C::BM) + 0.5);
+  return g < 1 ? 1 : g;
 }
 
 // Launch rows [row_begin, row_end) of a task (row_begin % BM == 0).
@@ -168,17 +176,17 @@ static cudaError_t launch2(Args2<typename C::T> a, cudaStream_t st, int64_t row_
   a.m_end = row_end;
   a.tiles_m = (row_end - row_begin + C::BM - 1) / C::BM;
   a.tiles_n = (a.n + C::BN - 1) / C::BN;
-  int64_t blocks;
+  a.band = band_height<C>();
+  a.nbands = (a.tiles_m + a.band - 1) / a.band;
+  int64_t blocks = 0;
+  for (int64_t b = 0; b < a.nbands; ++b)
+    blocks += band_count(b, a.band, a.row_tile0, a.tiles_m, a.tiles_n, C::BM, C::BN, a.diagonal);
   int64_t* pref = nullptr;
-  if (a.diagonal) {
-    blocks = diag_tiles<C>(a.tiles_m, a.row_tile0, a.tiles_n);
-    e = cudaMallocAsync(&pref, (a.tiles_m + 1) * sizeof(int64_t), st);
-    if (e != cudaSuccess) return e;
-    k_diag_prefix<<<1, 1024, 0, st>>>(a.tiles_m, a.row_tile0, a.tiles_n, C::BM, C::BN, pref);
-    a.row_pref = pref;
-  } else {
-    blocks = a.tiles_m * a.tiles_n;
-  }
+  e = cudaMallocAsync(&pref, (a.nbands + 1) * sizeof(int64_t), st);
+  if (e != cudaSuccess) return e;
+  k_band_prefix<<<1, 1024, 0, st>>>(a.nbands, a.band, a.row_tile0, a.tiles_m, a.tiles_n, C::BM,
+                                    C::BN, a.diagonal, pref);
+  a.row_pref = pref;
   if (blocks > 0x7fffffffLL) e = cudaErrorInvalidConfiguration;
   else if (blocks > 0) k_minplus2<C, MODE><<<(unsigned)blocks, kNT, C::SMEM_BYTES, st>>>(a);
   if (e == cudaSuccess) e = cudaGetLastError();

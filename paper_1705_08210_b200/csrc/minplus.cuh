@@ -183,8 +183,16 @@ __device__ __forceinline__ void stage_load(typename C::T* st, const typename C::
     if (row < cols && bytes) src = V + row * ldv + q0; else bytes = 0;
     cp_async16(st + (C::BM + row) * C::PITCH + ch * C::VEC, src, bytes);
   }
-  if (PIVOT && tid < 8) {
-    const int64_t q0 = q_base + tid * C::VEC;
+}
+
+// Pivot chunk kt (3-way) into the pivot slot of stage buffer `st`.
+template <class C>
+__device__ __forceinline__ void pivot_load(typename C::T* st, const typename C::T* __restrict__ xj,
+                                           int64_t n_f, int kt) {
+  using T = typename C::T;
+  const int tid = threadIdx.x;
+  if (tid < 8) {
+    const int64_t q0 = (int64_t)kt * C::BK + tid * C::VEC;
     const int64_t rem = (n_f - q0) * (int64_t)sizeof(T);
     const int bytes = rem >= 16 ? 16 : (rem > 0 ? (int)rem : 0);
     cp_async16(st + (C::BM + C::BN) * C::PITCH + tid * C::VEC, bytes ? xj + q0 : xj, bytes);
@@ -194,10 +202,11 @@ __device__ __forceinline__ void stage_load(typename C::T* st, const typename C::
 // 3-way prologue on a landed stage: A[r][q] <- min(x_j[q], A[r][q])
 // (xj_columns, mingemm.py:225-234). min is exact, so the later sum of
 // min(X, V_k) equals sum_q min(min(x_j, v_i), v_k) bit for bit (Appendix C r8).
+// Runs after the stage's barrier; each thread rewrites the A chunks its own
+// cp.asyncs brought in, with the stage's pivot chunk `xs`.
 template <class C>
-__device__ __forceinline__ void stage_pivot_min(typename C::T* st) {
+__device__ __forceinline__ void stage_pivot_min(typename C::T* st, const typename C::T* xs) {
   using T = typename C::T;
-  const T* xs = st + (C::BM + C::BN) * C::PITCH;
   const int tid = threadIdx.x;
 #pragma unroll
   for (int r = 0; r < (C::BM * 8) / kNT; ++r) {
@@ -234,10 +243,13 @@ __device__ __forceinline__ void minplus_tile(const typename C::T* __restrict__ W
     for (int n = 0; n < C::TN; ++n) acc[m][n] = T(0);
 
   const int KT = (int)((n_f + C::BK - 1) / C::BK);
+  constexpr int XS = (C::BM + C::BN) * C::PITCH;  // pivot slot offset inside a stage
 #pragma unroll
   for (int s = 0; s < S - 1; ++s) {
-    if (s < KT)
+    if (s < KT) {
       stage_load<C, PIVOT>(smem + s * C::STAGE_ELEMS, W, ldw, rows, V, ldv, cols, xj, n_f, s);
+      if (PIVOT) pivot_load<C>(smem + s * C::STAGE_ELEMS, xj, n_f, s);
+    }
     cp_async_commit();
   }
   for (int kt = 0; kt < KT; ++kt) {
@@ -245,13 +257,17 @@ __device__ __forceinline__ void minplus_tile(const typename C::T* __restrict__ W
     __syncthreads();
     T* st = smem + (kt % S) * C::STAGE_ELEMS;
     if (PIVOT) {
-      stage_pivot_min<C>(st);
+      // (measured: transforming own chunks before the barrier with the pivot
+      // staged one group early was 3% slower than this extra barrier)
+      stage_pivot_min<C>(st, st + XS);
       __syncthreads();
     }
     const int nk = kt + S - 1;
-    if (nk < KT)
+    if (nk < KT) {
       stage_load<C, PIVOT>(smem + (nk % S) * C::STAGE_ELEMS, W, ldw, rows, V, ldv, cols, xj,
                            n_f, nk);
+      if (PIVOT) pivot_load<C>(smem + (nk % S) * C::STAGE_ELEMS, xj, n_f, nk);
+    }
     cp_async_commit();
     const T* As = st;
     const T* Bs = st + C::BM * C::PITCH;
@@ -259,6 +275,39 @@ __device__ __forceinline__ void minplus_tile(const typename C::T* __restrict__ W
     for (int kk = 0; kk < C::BK; kk += C::VEC) micro_step<C>(acc, As, Bs, ty, tx, kk);
   }
   cp_async_wait<0>();
+}
+
+// First column tile of row-tile b in a diagonal task (the tile holding
+// column b*BM + 1: every tile with some i < j); 0 for rectangles.
+__host__ __device__ __forceinline__ int64_t first_col_tile(int64_t b, int64_t bm, int64_t bn,
+                                                           int diagonal) {
+  return diagonal ? (b * bm + 1) / bn : 0;
+}
+
+// Banded rasterisation: row-tiles are grouped in bands of G; inside a band
+// tiles run column-major (all G rows of one column tile, then the next), so
+// the CTAs resident at the same time share ~G row panels and ~W/G column
+// panels in L2 instead of one row panel and W column panels (W = resident
+// CTAs). band_pref[b] = tiles before band b; in a diagonal band the tiles
+// left of a row's first column are enumerated too and skipped (returns
+// false) -- at most G(G-1)/2 empty CTAs per band.
+__device__ __forceinline__ bool band_tile(int64_t t, const int64_t* __restrict__ band_pref,
+                                          int64_t nbands, int64_t G, int64_t row_tile0,
+                                          int64_t row_tile_end, int64_t bm, int64_t bn,
+                                          int diagonal, int& bi, int& bj) {
+  int64_t lo = 0, hi = nbands;
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (band_pref[mid] <= t) lo = mid; else hi = mid;
+  }
+  const int64_t r0 = row_tile0 + lo * G;
+  const int64_t rows = min64(G, row_tile_end - r0);
+  const int64_t u = t - band_pref[lo];
+  const int64_t b = r0 + u % rows;
+  const int64_t c = first_col_tile(r0, bm, bn, diagonal) + u / rows;
+  bi = (int)b;
+  bj = (int)c;
+  return c >= first_col_tile(b, bm, bn, diagonal);
 }
 
 // Diagonal-block tile enumeration: row-tile b holds the column tiles from

@@ -366,28 +366,32 @@ class Runner3Dist:
 
 class Resident3:
     """Benchmark harness for one GPU: input, sums and the 2-way numerator table
-    stay resident; each step runs every box of the single-slab plan stage by
-    stage (n_st chosen so one stage's values fit ``out_budget`` bytes), writing
-    all values to a reused HBM stage buffer and accumulating the checksum."""
+    stay resident; each step runs the whole single-slab tetrahedron as boxes
+    over consecutive pivot ranges J (each box's values fit ``out_budget``
+    bytes), writing all values to a reused HBM buffer and accumulating the
+    checksum. Pivot-range boxes keep the full k extent, so tiles are less
+    ragged than the reference's k-sliced stages (plan.stage_range)."""
 
     kernel_name = "k_czek3<T> (psim_czek3_box)"
 
     def __init__(self, problem, grid, out_budget: float = 40e9):
-        from .domain import n_ranks
+        from .domain import DecompGrid, n_ranks
 
         if n_ranks(grid) != 1:
             raise ValueError("Resident3 runs a single-rank grid")
         self.problem = problem
         n, isz = problem.n_v, (8 if problem.precision == "double" else 4)
-        total = n * (n - 1) * (n - 2) // 6 * isz
-        n_st = 1
-        while total / n_st > out_budget or (n // 6) % n_st:
-            n_st += 1
-            if n_st > n // 6:
-                raise ConfigError("no stage count fits the output budget")
-        from .domain import DecompGrid
-
-        self.grid = DecompGrid(n_st=n_st)
+        cap = max(1, int(out_budget // isz))
+        chunks, j0, cnt = [], 0, 0
+        for j in range(n):
+            c = j * (n - 1 - j)
+            if cnt + c > cap and j > j0:
+                chunks.append((j0, j))
+                j0, cnt = j, 0
+            cnt += c
+        chunks.append((j0, n))
+        self.chunks = chunks
+        self.grid = DecompGrid()
         self.code = D.code_of(problem.precision)
         self.kernel_cmp_per_launch = None
         self.launches_per_step = None
@@ -401,14 +405,8 @@ class Resident3:
         self.tables = Tables(self.blocks, self.code)
         self.tables(0, 0)
         self.acc = D.new_acc(dev)
-        self.stage_boxes = []
-        n_vp = p.n_v
-        for s in range(g.n_st):
-            boxes = []
-            for ev in plan_3way(g, RankCoords(0, 0, 0)):
-                if isinstance(ev, Unit3):
-                    boxes.extend(unit_boxes(ev, n_vp, g.n_st, (s,)))
-            self.stage_boxes.append(merge_boxes(boxes))
+        n = p.n_v
+        self.stage_boxes = [[Box((0, 0, 0), 0, n, ja, jb, 0, n)] for ja, jb in self.chunks]
         sizes = []
         for boxes in self.stage_boxes:
             sizes.append(sum(box_plan(box_struct(b, self.blocks, self.sums, self.tables, p.n_f,
