@@ -234,5 +234,61 @@ def pair_values_sampled(V, pairs):
     return out
 
 
+def _seq_sum(x, slabs: int = 1):
+    """Sequential ascending sum from +0 (np.cumsum is a strict left-to-right
+    scan); with slabs > 1, per-slab sums folded in ascending slab order
+    (reduce_field_axis, engine.py:197-216)."""
+    x = np.asarray(x)
+    w = len(x) // slabs
+    total = None
+    for p in range(slabs):
+        part = np.cumsum(np.concatenate([np.zeros(1, x.dtype), x[p * w:(p + 1) * w]]))[-1]
+        total = part if total is None else total + part
+    return total
+
+
+def pair_values_sampled_slabs(V, pairs, n_pf: int = 1):
+    """Selected 2-way values recomputed from their two columns only."""
+    V = np.asarray(V)
+    dt = V.dtype.type
+    out = np.empty(len(pairs), dtype=V.dtype)
+    for t, (i, j) in enumerate(pairs):
+        a, b = V[:, i], V[:, j]
+        n = _seq_sum(np.where(a < b, a, b), n_pf)
+        d = _seq_sum(a, n_pf) + _seq_sum(b, n_pf)
+        out[t] = dt(0) if d == 0 else (dt(2) * n) / d
+    return out
+
+
+def triple_values_sampled(V, triples, n_pf: int = 1):
+    """Selected 3-way values recomputed from their three columns only
+    (pair_numerators / triple_min_numerators / metric3_value)."""
+    V = np.asarray(V)
+    dt = V.dtype.type
+    out = np.empty(len(triples), dtype=V.dtype)
+    for t, (i, j, k) in enumerate(triples):
+        a, b, c = V[:, i], V[:, j], V[:, k]
+        nij = _seq_sum(np.where(a < b, a, b), n_pf)
+        nik = _seq_sum(np.where(a < c, a, c), n_pf)
+        njk = _seq_sum(np.where(b < c, b, c), n_pf)
+        ab = np.where(a < b, a, b)
+        n3p = _seq_sum(np.where(ab < c, ab, c), n_pf)
+        d = (_seq_sum(a, n_pf) + _seq_sum(b, n_pf)) + _seq_sum(c, n_pf)
+        n3 = ((nij + nik) + njk) - n3p
+        out[t] = dt(0) if d == 0 else (dt(1.5) * n3) / d
+    return out
+
+
+def uniform_cols(seed: int, n_f: int, n_v: int, cols, dtype=np.float64):
+    """Selected global columns of the uniform matrix."""
+    q = np.arange(n_f, dtype=np.uint64)[:, None]
+    i = np.asarray(cols, dtype=np.uint64)[None, :]
+    with np.errstate(over="ignore"):
+        h = mix64((q * np.uint64(n_v) + i) ^ np.uint64(seed & MASK64))
+    if np.dtype(dtype) == np.float64:
+        return np.asfortranarray((h >> np.uint64(11)).astype(np.float64) * 2.0**-53)
+    return np.asfortranarray((h >> np.uint64(40)).astype(np.float32) * np.float32(2.0**-24))
+
+
 def n_pairs(n_v: int) -> int:
     return math.comb(n_v, 2)

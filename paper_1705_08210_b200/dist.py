@@ -186,7 +186,10 @@ class Runner2:
         self.my_cmp = sum(problem.n_f // grid.n_pf * D.pair_count(t.r1 - t.r0, t.c1 - t.c0,
                                                                    t.diagonal) for t in tasks)
         self.kernel_cmp_per_launch = self.my_cmp / max(1, len(tasks))
-        self.launches_per_step = 1 + len(tasks) * (1 if grid.n_pf == 1 else 2 + grid.n_pf)
+        # our kernels per step: column sums (+ field fold), then per task the
+        # band-prefix + min-plus launch (+ fold steps and the epilogue with a field split)
+        per_task = 2 if grid.n_pf == 1 else 2 + (grid.n_pf - 1) + 1
+        self.launches_per_step = 1 + (grid.n_pf - 1) + len(tasks) * per_task
 
     def peer(self, slab: int) -> int:
         c = self.coords
@@ -196,10 +199,13 @@ class Runner2:
         dev = torch.device("cuda", torch.cuda.current_device())
         self.dev = dev
         self.own = D.load_block(self.problem, self.grid, self.coords, dev)
+        # receive buffers: one per in-flight exchange (double buffering), none
+        # without a vector split (field-only grids hold just their own slab)
+        n_buf = min(2, sum(1 for e in self.events if isinstance(e, Exchange)))
         self.remote = [D.Block(torch.empty_like(self.own.data), self.own.n_fp, self.own.n_vp,
-                               self.own.ld, 0, self.problem.precision) for _ in range(2)]
+                               self.own.ld, 0, self.problem.precision) for _ in range(n_buf)]
         self.remote_sums = [torch.empty(self.n_vp, dtype=self.own.data.dtype, device=dev)
-                            for _ in range(2)]
+                            for _ in range(n_buf)]
         self.acc = D.new_acc(dev)
 
     def _sums(self) -> torch.Tensor:

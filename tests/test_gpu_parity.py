@@ -210,6 +210,96 @@ def test_large_2way_sampled_parity_and_properties():
     assert (vals[idx].view(np.uint64) == got.view(np.uint64)).all()
 
 
+def _sample(rng, n_v, count, arity):
+    out = set()
+    while len(out) < count:
+        t = tuple(sorted(int(x) for x in rng.choice(n_v, size=arity, replace=False)))
+        out.add(t)
+    return sorted(out)
+
+
+def _recompute(P, O, kind, seed, n_f, n_v, tuples, precision, n_pf=1, bits=20):
+    dt = np.float64 if precision == "double" else np.float32
+    cols = sorted({c for t in tuples for c in t})
+    pos = {c: p for p, c in enumerate(cols)}
+    if kind == "uniform":
+        V = O.uniform_cols(seed, n_f, n_v, cols, dt)
+    else:
+        V = O.random_exact_cols(seed, n_f, n_v, bits, cols, dt)
+    local = [tuple(pos[c] for c in t) for t in tuples]
+    if len(tuples[0]) == 2:
+        return O.pair_values_sampled_slabs(V, local, n_pf)
+    return O.triple_values_sampled(V, local, n_pf)
+
+
+def test_large_fp32_2way_sampled_uniform():
+    """cfg3's field width (n_f = 50000, FP32) on general FP data: sampled pairs
+    bitwise equal to the column-only sequential recompute; checksum equals the
+    checksum of the returned values."""
+    from oracle import propsim_np as O
+
+    P = _api()
+    n_f, n_v = 50000, 2048
+    res = P.run_2way(P.Problem(2, n_f, n_v, P.gen_uniform(3, n_f, n_v), "single"), P.DecompGrid())
+    vals = res.records.values
+    assert res.checksum.hex == O.checksum_hex(np.arange(len(vals)), vals)
+    pairs = _sample(np.random.default_rng(2), n_v, 300, 2)
+    got = _recompute(P, O, "uniform", 3, n_f, n_v, pairs, "single")
+    idx = [P.pair_index(i, j, n_v) for i, j in pairs]
+    assert (vals[idx].view(np.uint32) == got.view(np.uint32)).all()
+
+
+def test_large_3way_sampled_and_stage_tiling():
+    """cfg4's field width (n_f = 10000, FP64), n_v = 600 (3.6e7 triples):
+    sampled triples bitwise vs the column-only recompute; the two stages of
+    n_st = 2 partition the run and their checksums add up to the full one."""
+    from oracle import propsim_np as O
+
+    P = _api()
+    n_f, n_v = 10000, 600
+    prob = P.Problem(3, n_f, n_v, P.gen_uniform(21, n_f, n_v), "double")
+    full = P.run_3way(prob, P.DecompGrid())
+    vals = full.records.values
+    assert len(vals) == math.comb(n_v, 3)
+    assert full.checksum.hex == O.checksum_hex(np.arange(len(vals)), vals)
+    triples = _sample(np.random.default_rng(5), n_v, 200, 3)
+    got = _recompute(P, O, "uniform", 21, n_f, n_v, triples, "double")
+    idx = [P.triple_index(*t, n_v) for t in triples]
+    assert (vals[idx].view(np.uint64) == got.view(np.uint64)).all()
+    parts = [P.run_3way(prob, P.DecompGrid(n_st=2), stage=s, keep_values=False) for s in (0, 1)]
+    assert P.combine_checksums([p.checksum for p in parts]) == full.checksum
+    assert parts[0].records.__len__() + parts[1].records.__len__() == len(vals)
+
+
+def test_large_field_split_sampled():
+    """A cfg5-like deep field axis (n_f = 1,000,000 FP64) split over n_pf = 4
+    slabs (ordered fold): sampled pairs bitwise vs the per-slab recompute."""
+    from oracle import propsim_np as O
+
+    P = _api()
+    n_f, n_v = 1_000_000, 256
+    res = P.run_2way(P.Problem(2, n_f, n_v, P.gen_uniform(7, n_f, n_v), "double"),
+                     P.DecompGrid(n_pf=4))
+    vals = res.records.values
+    pairs = _sample(np.random.default_rng(9), n_v, 60, 2)
+    got = _recompute(P, O, "uniform", 7, n_f, n_v, pairs, "double", n_pf=4)
+    idx = [P.pair_index(i, j, n_v) for i, j in pairs]
+    assert (vals[idx].view(np.uint64) == got.view(np.uint64)).all()
+    assert res.checksum.hex == O.checksum_hex(np.arange(len(vals)), vals)
+
+
+def test_band_launches_equal_single_launch():
+    """host_values=True runs the diagonal task as row bands with overlapped
+    D2H copies; values and checksum must equal the single-launch run."""
+    P = _api()
+    spec = P.gen_uniform(4, 3000, 3000)
+    prob = P.Problem(2, 3000, 3000, spec, "double")
+    a = P.run_2way(prob, P.DecompGrid())
+    b = P.run_2way(prob, P.DecompGrid(), host_values=True)
+    assert a.checksum == b.checksum
+    assert (a.records.values.view(np.uint64) == b.records.values.view(np.uint64)).all()
+
+
 def test_data_errors_on_device():
     P = _api()
     m = np.ones((4, 4))
