@@ -26,6 +26,8 @@
 //   FP32: FMNMX + half an FADD2 (packed f32x2 add over two accumulators)
 #pragma once
 
+#include <type_traits>
+
 #include "psim_common.cuh"
 #include "psim_internal.h"
 
@@ -206,15 +208,27 @@ __device__ __forceinline__ void pivot_load(typename C::T* st, const typename C::
 // cp.asyncs brought in, with the stage's pivot chunk `xs`.
 template <class C>
 __device__ __forceinline__ void stage_pivot_min(typename C::T* st, const typename C::T* xs) {
-  using T = typename C::T;
+  // 16-byte vector accesses: a warp's 8 consecutive lanes cover one row's
+  // 128 B (distinct banks), so the rewrite is conflict-free.
+  using V4 = typename std::conditional<sizeof(typename C::T) == 8, double2, float4>::type;
   const int tid = threadIdx.x;
+  const int ch = tid & 7;  // the same chunk column for all of this thread's rows
+  const V4 x = *reinterpret_cast<const V4*>(xs + ch * C::VEC);
 #pragma unroll
   for (int r = 0; r < (C::BM * 8) / kNT; ++r) {
-    const int c = tid + r * kNT;
-    const int row = c >> 3, ch = c & 7;
-    T* p = st + row * C::PITCH + ch * C::VEC;
-#pragma unroll
-    for (int v = 0; v < C::VEC; ++v) p[v] = Traits<T>::min(xs[ch * C::VEC + v], p[v]);
+    const int row = (tid + r * kNT) >> 3;
+    V4* p = reinterpret_cast<V4*>(st + row * C::PITCH + ch * C::VEC);
+    V4 a = *p;
+    if constexpr (sizeof(typename C::T) == 8) {
+      a.x = Traits<double>::min(x.x, a.x);
+      a.y = Traits<double>::min(x.y, a.y);
+    } else {
+      a.x = Traits<float>::min(x.x, a.x);
+      a.y = Traits<float>::min(x.y, a.y);
+      a.z = Traits<float>::min(x.z, a.z);
+      a.w = Traits<float>::min(x.w, a.w);
+    }
+    *p = a;
   }
 }
 
