@@ -265,8 +265,9 @@ def run_ours(args) -> dict | None:
     achieved = kern_cmp / (kern_ms * 1e-3) if kern_ms > 0 else None
     traffic = None
     prof = ROOT / "profiles" / "ncu_traffic.json"
-    if prof.exists():
-        traffic = json.loads(prof.read_text()).get(f"{args.config}:{world}")
+    if prof.exists():  # measured once with ncu (bytes per launch), see profiles/
+        entry = json.loads(prof.read_text()).get(f"{args.config}:{world}")
+        traffic = entry.get("bytes") if isinstance(entry, dict) else entry
 
     # end-to-end through the public API with host buffers
     e2e = None
