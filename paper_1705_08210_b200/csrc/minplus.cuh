@@ -85,6 +85,9 @@ template <class C>
 __device__ __forceinline__ void micro_step(double (&acc)[C::TM][C::TN], const double* As,
                                            const double* Bs, int ty, int tx, int kk) {
   constexpr int P = C::PITCH;
+  // (measured alternatives, profiles/r01_tile_sweep.jsonl: B-stationary
+  // register tiles and per-element q pairs are no faster; the FP64 mix tops
+  // out near 21.3 cmp/clk/SM for every tile shape)
   double2 a[C::TM];
 #pragma unroll
   for (int m = 0; m < C::TM; ++m)

@@ -91,14 +91,8 @@ void run(const char* name, int64_t n, int64_t n_f) {
 int main(int argc, char** argv) {
   int64_t n = argc > 1 ? atoll(argv[1]) : 8192;
   int64_t nf = argc > 2 ? atoll(argv[2]) : 20000;
-  run<Cfg<double, 8, 8, 4, 1>>("f64_8x8_s4", n, nf);
-  run<Cfg<float, 8, 8, 4, 1, 0>>("f32_8x8_s4_v0", n, nf * 5 / 2);
-  run<Cfg<float, 8, 8, 4, 1, 1>>("f32_8x8_s4_v1", n, nf * 5 / 2);
-  run<Cfg<float, 8, 8, 4, 1, 2>>("f32_8x8_s4_v2", n, nf * 5 / 2);
-  run<Cfg<float, 8, 8, 4, 1, 3>>("f32_8x8_s4_v3", n, nf * 5 / 2);
-  run<Cfg<float, 16, 8, 3, 1, 1>>("f32_16x8_s3_v1", n, nf * 5 / 2);
-  run<Cfg<float, 16, 8, 3, 1, 3>>("f32_16x8_s3_v3", n, nf * 5 / 2);
-  run<Cfg<float, 8, 4, 3, 2, 1>>("f32_8x4_s3_b2_v1", n, nf * 5 / 2);
-  run<Cfg<float, 8, 4, 3, 2, 3>>("f32_8x4_s3_b2_v3", n, nf * 5 / 2);
+  run<Cfg<double, 8, 8, 4, 1, 0>>("f64_8x8_s4_v0", n, nf);
+  run<Cfg<double, 16, 4, 3, 1, 0>>("f64_16x4_s3_v0", n, nf);
+  run<Cfg<double, 4, 16, 3, 1, 0>>("f64_4x16_s3_v0", n, nf);
   return 0;
 }
