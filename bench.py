@@ -271,9 +271,9 @@ def run_ours(args) -> dict | None:
 
     # end-to-end through the public API with host buffers
     e2e = None
-    if not args.no_e2e and world == 1 and arity == 2:
-        e2e = e2e_2way(P, prob, n_f, n_v, precision, args, total_cmp)
     runner.teardown()
+    if not args.no_e2e and arity == 2:
+        e2e = e2e_2way(P, prob, grid, precision, args, total_cmp, world, rank)
 
     line = None
     if rank == 0:
@@ -331,55 +331,66 @@ def run_ours(args) -> dict | None:
     return line
 
 
-def e2e_2way(P, prob, n_f, n_v, precision, args, total_cmp) -> dict:
-    """run_2way through the public API, inputs in pinned host memory."""
+def e2e_2way(P, prob, grid, precision, args, total_cmp, world, rank) -> dict:
+    """run_2way through the public API with this rank's input slab in pinned
+    host memory: every step copies the slab H2D, runs, and streams every value
+    this rank owns back D2H (host_values=True), plus the checksum gather.
+    Wall time per step, max over ranks."""
     import torch
+    import torch.distributed as dist
 
-    tdt = torch.float64 if precision == "double" else torch.float32
-    host = torch.empty((n_v, n_f), dtype=tdt, pin_memory=True)  # Fortran (n_f, n_v) bytes
     from paper_1705_08210_b200 import device as D
+    from paper_1705_08210_b200.domain import coords_of_rank
 
-    # fill the host buffer with the same synthetic matrix (generated on device, copied once)
-    blk = D.load_block(prob, P.DecompGrid(), P.RankCoords(0, 0, 0), torch.device("cuda"))
-    host.copy_(blk.data[:, :n_f])
+    coords = coords_of_rank(rank, grid)
+    blk = D.load_block(prob, grid, coords, torch.device("cuda"))  # same synthetic slab
+    host = torch.empty((blk.n_vp, blk.n_fp), dtype=blk.data.dtype, pin_memory=True)
+    host.copy_(blk.data[:, :blk.n_fp])
     del blk
-    src = PinnedSource(host.numpy().T)
-    e2e_prob = P.Problem(2, n_f, n_v, src, precision)
+    src = SlabSource(host.numpy().T, coords)
+    e2e_prob = P.Problem(2, prob.n_f, prob.n_v, src, precision)
+    transport = "nccl" if world > 1 else "local"
     steps = max(1, min(args.steps, 3))
-    res = P.run_2way(e2e_prob, P.DecompGrid(), host_values=True)  # warm-up (allocations)
-    _ = res.records.values
-    del res
+
+    def once():
+        res = P.run_2way(e2e_prob, grid, transport=transport, host_values=True)
+        if world == 1:
+            _ = res.records.values  # canonical host array (already copied during the run)
+        return res.checksum.hex
+
+    once()  # warm-up (allocations, pinned host buffers)
     times = []
     for _ in range(steps):
+        if world > 1:
+            dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        res = P.run_2way(e2e_prob, P.DecompGrid(), host_values=True)
-        vals = res.records.values  # every value, copied D2H band by band during the run
-        cks = res.checksum.hex
-        t1 = time.perf_counter()
-        times.append(t1 - t0)
-        del res, vals
+        cks = once()
+        times.append(time.perf_counter() - t0)
     el = statistics.median(times)
+    if world > 1:
+        t = torch.tensor([el], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el = float(t.item())
     isz = 8 if precision == "double" else 4
     return {"value": total_cmp / el, "unit": "comparisons/s",
-            "h2d_bytes_per_step": n_f * n_v * isz,
-            "d2h_bytes_per_step": math.comb(n_v, 2) * isz + 24,
+            "h2d_bytes_per_step": prob.n_f * prob.n_v * isz,
+            "d2h_bytes_per_step": math.comb(prob.n_v, 2) * isz + 32 * world,
             "seconds_per_step": el, "checksum": cks,
-            "api": "paper_1705_08210_b200.run_2way(Problem(2, n_f, n_v, pinned ArraySource), host_values=True)"}
+            "api": f"paper_1705_08210_b200.run_2way(Problem(2, n_f, n_v, pinned slab source), "
+                   f"grid, transport='{transport}', host_values=True)"}
 
 
-class PinnedSource:
-    """ArraySource over one pinned host matrix (reference tests/conftest.py:17-26)."""
+class SlabSource:
+    """One rank's input slab in pinned host memory (an ArraySource restricted
+    to the caller's own block, reference tests/conftest.py:17-26)."""
 
-    def __init__(self, matrix):
-        self.matrix = matrix
+    def __init__(self, matrix, coords):
+        self.matrix, self.coords = matrix, tuple(coords)
 
     def local_block(self, problem, grid, coords):
-        from paper_1705_08210_b200.domain import field_range, vector_range
-
-        f0, f1 = field_range(grid, coords.p_f, problem.n_f)
-        v0, v1 = vector_range(grid, coords.p_v, problem.n_v)
-        return self.matrix[f0:f1, v0:v1]
+        assert tuple(coords) == self.coords, "slab source holds one rank's block"
+        return self.matrix
 
 
 # ---------------------------------------------------------------------------

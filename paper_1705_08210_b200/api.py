@@ -152,7 +152,8 @@ def run_2way(problem, grid, *, transport: str = "local", kernel: str | None = No
     if mode == "nccl":
         from . import dist
 
-        out = dist.run_2way_nccl(problem, grid, balance=balance, keep_values=keep_values)
+        out = dist.run_2way_nccl(problem, grid, balance=balance, keep_values=keep_values,
+                                 host_values=host_values)
     else:
         out = engine2.run_local(problem, grid, balance=balance, keep_values=keep_values,
                                 host_values=host_values)

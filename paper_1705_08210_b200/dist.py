@@ -29,7 +29,7 @@ import torch.distributed as dist
 
 from . import device as D
 from .domain import ConfigError, RankCoords, coords_of_rank, n_ranks, rank_of_coords
-from .engine2 import Outcome, finish_numerators
+from .engine2 import HostSink, Outcome, finish_numerators, run_task
 from .plan import Exchange, Task2, plan_2way
 from .records import PairPiece
 
@@ -174,9 +174,11 @@ class Runner2:
 
     kernel_name = "k_minplus2<T, kCzek2> (psim_czek2_block)"
 
-    def __init__(self, problem, grid, balance: str = "split", keep_values: bool = True):
+    def __init__(self, problem, grid, balance: str = "split", keep_values: bool = True,
+                 host_values: bool = False):
         self.world, self.rank = ensure_initialized(grid)
         self.problem, self.grid, self.balance, self.keep = problem, grid, balance, keep_values
+        self.sink = HostSink() if host_values else None
         self.coords = coords_of_rank(self.rank, grid)
         self.code = D.code_of(problem.precision)
         self.n_vp = problem.n_v // grid.n_pv
@@ -273,20 +275,23 @@ class Runner2:
         tdt = D.torch_dtype(p.precision)
         W = self.own
         if g.n_pf == 1:
-            vals = torch.empty(count, dtype=tdt, device=self.dev) if self.keep else None
-            D.czek2_block(self.code, W, t.r0, t.r1, V, t.c0, t.c1, s_row, s_col, t.diagonal,
-                          p.n_v, vals, self.acc)
-            return [PairPiece(W.v0 + t.r0, V.v0 + t.c0, m, n, t.diagonal, 0, m, vals)]
+            return [run_task(self.code, p, g, t, [W], [V], s_row, s_col, self.acc, self.keep,
+                             self.sink)]
         # field split: partial packed numerators -> all-to-all row chunks -> ordered fold
         part = torch.empty(count, dtype=tdt, device=self.dev)
         D.mgemm_packed(self.code, W, t.r0, t.r1, V, t.c0, t.c1, t.diagonal, part)
         total, r0, r1 = reduce_scatter_rows(part, m, n, t.diagonal, self.coords.p_f, g.n_pf,
                                             self.group,
                                             lambda dst, src: D.fold_(dst, src, self.code))
-        vals = torch.empty(total.numel(), dtype=tdt, device=self.dev) if self.keep else None
+        keep = self.keep or self.sink is not None
+        vals = torch.empty(total.numel(), dtype=tdt, device=self.dev) if keep else None
         if r1 > r0:
             finish_numerators(self.code, total, r0, r1, m, n, t.diagonal, s_row[t.r0:],
                               s_col[t.c0:], W.v0 + t.r0, V.v0 + t.c0, p.n_v, vals, self.acc)
+        if self.sink is not None:
+            host = self.sink.buffer(vals.numel(), tdt)
+            self.sink.copy(host, vals, 0, vals.numel())
+            vals = host
         return [PairPiece(W.v0 + t.r0, V.v0 + t.c0, m, n, t.diagonal, r0, r1, vals)]
 
     def checksum_hex(self) -> str:
@@ -318,14 +323,17 @@ class Runner2:
         torch.cuda.empty_cache()
 
 
-def run_2way_nccl(problem, grid, balance: str = "split", keep_values: bool = True) -> Outcome:
-    r = Runner2(problem, grid, balance, keep_values)
-    r.setup()
+def run_2way_nccl(problem, grid, balance: str = "split", keep_values: bool = True,
+                  host_values: bool = False) -> Outcome:
+    r = Runner2(problem, grid, balance, keep_values, host_values)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record()
+    r.setup()
     r.step()
     end.record()
     end.synchronize()
+    if r.sink is not None:
+        r.sink.finish()
     el = torch.tensor([start.elapsed_time(end) * 1e-3], dtype=torch.float64, device=r.dev)
     dist.all_reduce(el, op=dist.ReduceOp.MAX)
     lo, hi, deg, cnt = r.totals()
