@@ -138,6 +138,10 @@ int psim_mgemm(int dtype, const void* W, int64_t ldw, const void* V, int64_t ldv
                void* stream);
 /* Fused 2-way block task (see psim_block2_t). */
 int psim_czek2_block(int dtype, const psim_block2_t* task, void* stream);
+/* Several tasks of one rank (same dtype, n_f, n_v) in a single grid, so the
+ * circulant steps of a slab share one launch and one tail (metrics2.py:148-158
+ * over the plan of schedule.py:116-142). */
+int psim_czek2_tasks(int dtype, const psim_block2_t* tasks, int ntasks, void* stream);
 /* 2-way epilogue from reduced packed numerators, rows [r0, r1) of a task's
  * packed layout (field-axis path, metrics2.py:156-158). N and vals point at
  * the first entry of row r0. */

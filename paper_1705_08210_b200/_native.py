@@ -72,6 +72,7 @@ SIGNATURES = {
         [C.c_int, c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64, C.c_int, c_vp, c_i64, C.c_int,
          c_vp]),
     "psim_czek2_block": (C.c_int, [C.c_int, C.POINTER(Block2), c_vp]),
+    "psim_czek2_tasks": (C.c_int, [C.c_int, C.POINTER(Block2), C.c_int, c_vp]),
     "psim_czek2_from_numerators": (
         C.c_int,
         [C.c_int, c_vp, c_i64, c_i64, c_i64, c_i64, C.c_int, c_vp, c_vp, c_i64, c_i64, c_i64,

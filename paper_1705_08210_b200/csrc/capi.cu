@@ -158,7 +158,24 @@ int psim_mgemm(int dtype, const void* W, int64_t ldw, const void* V, int64_t ldv
                      "psim_mgemm");
 }
 
+static int check_task2(int dtype, const psim_block2_t* t);
+
 int psim_czek2_block(int dtype, const psim_block2_t* t, void* stream) {
+  if (int r = check_task2(dtype, t)) return r;
+  return cuda_status(psim::czek2_block(dtype, *t, S(stream)), "psim_czek2_block");
+}
+
+int psim_czek2_tasks(int dtype, const psim_block2_t* tasks, int ntasks, void* stream) {
+  if (ntasks < 0 || (ntasks && !tasks)) return fail(PSIM_ECONFIG, "bad task list");
+  for (int k = 0; k < ntasks; ++k) {
+    if (int r = check_task2(dtype, tasks + k)) return r;
+    if (tasks[k].n_f != tasks[0].n_f || tasks[k].n_v != tasks[0].n_v)
+      return fail(PSIM_ECONFIG, "tasks of one launch must share n_f and n_v");
+  }
+  return cuda_status(psim::czek2_tasks(dtype, tasks, ntasks, S(stream)), "psim_czek2_tasks");
+}
+
+static int check_task2(int dtype, const psim_block2_t* t) {
   if (int r = check_dtype(dtype)) return r;
   if (!t) return fail(PSIM_ECONFIG, "task is NULL");
   if (t->n_f < 0 || t->m < 0 || t->n < 0) return fail(PSIM_ECONFIG, "negative extent");
@@ -175,7 +192,7 @@ int psim_czek2_block(int dtype, const psim_block2_t* t, void* stream) {
   if (t->row_begin < 0 || re > t->m || t->row_begin > re || t->row_begin % bm)
     return fail(PSIM_ECONFIG, "row band [%lld, %lld) invalid (begin must be a multiple of %d)",
                 (long long)t->row_begin, (long long)re, bm);
-  return cuda_status(psim::czek2_block(dtype, *t, S(stream)), "psim_czek2_block");
+  return PSIM_OK;
 }
 
 int psim_czek2_from_numerators(int dtype, const void* N, int64_t r0, int64_t r1, int64_t m,

@@ -34,6 +34,8 @@ cudaError_t column_sums(int dtype, const void* V, int64_t n_fp, int64_t n_vp, in
 cudaError_t fold_add(int dtype, void* dst, const void* src, int64_t count, cudaStream_t st);
 
 cudaError_t czek2_block(int dtype, const Czek2Block& t, cudaStream_t st);
+// Several 2-way tasks (same n_f, n_v, dtype) in one grid (<= 16 per launch).
+cudaError_t czek2_tasks(int dtype, const Czek2Block* tasks, int ntasks, cudaStream_t st);
 cudaError_t mgemm(int dtype, const void* W, int64_t ldw, const void* V, int64_t ldv, int64_t n_f,
                   int64_t m, int64_t n, int symmetric, void* M, int64_t ldm, int packed,
                   cudaStream_t st);

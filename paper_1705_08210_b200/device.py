@@ -161,6 +161,21 @@ def czek2_block(code: int, W: Block, r0: int, r1: int, V: Block, c0: int, c1: in
     N.call("psim_czek2_block", code, C.byref(t), stream_ptr())
 
 
+def czek2_tasks(code: int, specs: list, n_v: int, acc: torch.Tensor) -> None:
+    """Several fused 2-way tasks in one grid. specs: (W, r0, r1, V, c0, c1,
+    s_row, s_col, diagonal, vals) tuples sharing n_f."""
+    arr = (N.Block2 * len(specs))()
+    for k, (W, r0, r1, V, c0, c1, s_row, s_col, diagonal, vals) in enumerate(specs):
+        arr[k] = N.Block2(
+            W=W.col_ptr(r0), ldw=W.ld, V=V.col_ptr(c0), ldv=V.ld, n_f=W.n_fp,
+            m=r1 - r0, n=c1 - c0, diagonal=1 if diagonal else 0, row_begin=0, row_end=0,
+            s_row=s_row.data_ptr() + r0 * s_row.element_size(),
+            s_col=s_col.data_ptr() + c0 * s_col.element_size(),
+            g_row=W.v0 + r0, g_col=V.v0 + c0, n_v=n_v, vals=ptr(vals), acc=ptr(acc),
+        )
+    N.call("psim_czek2_tasks", code, arr, len(specs), stream_ptr())
+
+
 def mgemm_packed(code: int, W: Block, r0: int, r1: int, V: Block, c0: int, c1: int,
                  diagonal: bool, out: torch.Tensor) -> None:
     N.call("psim_mgemm", code, W.col_ptr(r0), W.ld, V.col_ptr(c0), V.ld, W.n_fp, r1 - r0, c1 - c0,

@@ -179,6 +179,9 @@ class Runner2:
         self.world, self.rank = ensure_initialized(grid)
         self.problem, self.grid, self.balance, self.keep = problem, grid, balance, keep_values
         self.sink = HostSink() if host_values else None
+        # fused: the diagonal task runs while every block exchange is in flight,
+        # then all remaining tasks of the slab share one grid (no per-task tail)
+        self.fused = grid.n_pf == 1 and not host_values
         self.coords = coords_of_rank(self.rank, grid)
         self.code = D.code_of(problem.precision)
         self.n_vp = problem.n_v // grid.n_pv
@@ -187,11 +190,17 @@ class Runner2:
         tasks = [e for e in self.events if isinstance(e, Task2)]
         self.my_cmp = sum(problem.n_f // grid.n_pf * D.pair_count(t.r1 - t.r0, t.c1 - t.c0,
                                                                    t.diagonal) for t in tasks)
-        self.kernel_cmp_per_launch = self.my_cmp / max(1, len(tasks))
-        # our kernels per step: column sums (+ field fold), then per task the
-        # band-prefix + min-plus launch (+ fold steps and the epilogue with a field split)
-        per_task = 2 if grid.n_pf == 1 else 2 + (grid.n_pf - 1) + 1
-        self.launches_per_step = 1 + (grid.n_pf - 1) + len(tasks) * per_task
+        # our kernels per step: column sums (+ field fold), then the min-plus
+        # grids: fused mode one for the diagonal task and one for all others;
+        # a field split runs per task min-plus + (n_pf - 1) folds + epilogue
+        if self.fused:
+            grids = int(any(t.diagonal for t in tasks)) + int(any(not t.diagonal for t in tasks))
+            self.launches_per_step = 1 + grids
+        else:
+            grids = len(tasks)
+            per_task = 1 if grid.n_pf == 1 else 1 + (grid.n_pf - 1) + 1
+            self.launches_per_step = 1 + (grid.n_pf - 1) + len(tasks) * per_task
+        self.kernel_cmp_per_launch = self.my_cmp / max(1, grids)
 
     def peer(self, slab: int) -> int:
         c = self.coords
@@ -201,9 +210,11 @@ class Runner2:
         dev = torch.device("cuda", torch.cuda.current_device())
         self.dev = dev
         self.own = D.load_block(self.problem, self.grid, self.coords, dev)
-        # receive buffers: one per in-flight exchange (double buffering), none
-        # without a vector split (field-only grids hold just their own slab)
-        n_buf = min(2, sum(1 for e in self.events if isinstance(e, Exchange)))
+        # receive buffers: fused mode keeps every received block (all exchanges
+        # in flight at once, one multi-task grid after them); otherwise one per
+        # in-flight exchange (double buffering). None without a vector split.
+        n_ex = sum(1 for e in self.events if isinstance(e, Exchange))
+        n_buf = n_ex if self.fused else min(2, n_ex)
         self.remote = [D.Block(torch.empty_like(self.own.data), self.own.n_fp, self.own.n_vp,
                                self.own.ld, 0, self.problem.precision) for _ in range(n_buf)]
         self.remote_sums = [torch.empty(self.n_vp, dtype=self.own.data.dtype, device=dev)
@@ -225,11 +236,57 @@ class Runner2:
         ]
         return dist.batch_isend_irecv(ops)
 
+    def _step_fused(self, s_own, timed: bool) -> list:
+        p = self.problem
+        tdt = D.torch_dtype(p.precision)
+        exchanges = [e for e in self.events if isinstance(e, Exchange)]
+        works = []
+        slot_of = {}
+        for k, ev in enumerate(exchanges):
+            slot_of[ev.step] = k
+            self.remote[k].v0 = ((self.coords.p_v + ev.step) % self.grid.n_pv) * self.n_vp
+            works.extend(self._post_exchange(ev, k, s_own))
+        tasks = [e for e in self.events if isinstance(e, Task2)]
+        diag = [t for t in tasks if t.diagonal]
+        rest = [t for t in tasks if not t.diagonal]
+        events, pieces = [], []
+
+        def grid_of(ts, blocks):
+            specs = []
+            for t, (V, s_col) in zip(ts, blocks):
+                m, n = t.r1 - t.r0, t.c1 - t.c0
+                vals = torch.empty(D.pair_count(m, n, t.diagonal), dtype=tdt,
+                                   device=self.dev) if self.keep else None
+                specs.append((self.own, t.r0, t.r1, V, t.c0, t.c1, s_own, s_col, t.diagonal,
+                              vals))
+                pieces.append(PairPiece(self.own.v0 + t.r0, V.v0 + t.c0, m, n, t.diagonal, 0, m,
+                                        vals))
+            if not specs:
+                return
+            if timed:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+            D.czek2_tasks(self.code, specs, p.n_v, self.acc)
+            if timed:
+                e1.record()
+                events.append((e0, e1))
+
+        grid_of(diag, [(self.own, s_own)] * len(diag))  # overlaps the exchanges
+        for w in works:
+            w.wait()
+        grid_of(rest, [(self.remote[slot_of[t.step]], self.remote_sums[slot_of[t.step]])
+                       for t in rest])
+        self.pieces = pieces
+        self.s_own = s_own
+        return events
+
     def step(self, timed: bool = False) -> list:
         """Run this rank's whole plan once; returns (start, end) kernel events."""
         p, g = self.problem, self.grid
         self.acc.zero_()
         s_own = self._sums()
+        if self.fused:
+            return self._step_fused(s_own, timed)
         pieces, events = [], []
         evs = list(self.events)
         exchanges = [e for e in evs if isinstance(e, Exchange)]

@@ -174,7 +174,7 @@ class Resident2:
             raise ValueError("Resident2 runs a single-rank grid")
         self.problem, self.grid = problem, grid
         self.code = D.code_of(problem.precision)
-        self.launches_per_step = 3  # column sums, band prefix, fused min-plus kernel
+        self.launches_per_step = 2  # column sums, fused min-plus kernel
         n = problem.n_v
         self.kernel_cmp_per_launch = problem.n_f * (n * (n - 1) // 2)
 

@@ -226,8 +226,8 @@ class Runner3Dist:
         work = sum(box_count(b) for b in self.edge_boxes + self.rest_boxes)
         self.my_cmp = work * problem.n_f
         self.kernel_cmp_per_launch = self.my_cmp / max(1, nb)
-        # column sums, (prefix + box) per box, (prefix + min-plus) per numerator table
-        self.launches_per_step = 1 + 2 * nb + 2 * (grid.n_pv * (grid.n_pv + 1) // 2)
+        # column sums, (prefix + box) per box, one min-plus per numerator table
+        self.launches_per_step = 1 + 2 * nb + grid.n_pv * (grid.n_pv + 1) // 2
 
     def peer(self, slab: int) -> int:
         from .domain import rank_of_coords
@@ -414,7 +414,7 @@ class Resident3:
                                                  p.n_v, None, self.acc))[0] for b in boxes))
         self.buf = torch.empty(max(sizes), dtype=D.torch_dtype(p.precision), device=dev)
         launches = sum(len(b) for b in self.stage_boxes)
-        self.launches_per_step = 3 + 2 * launches  # sums, N2 table (2), (prefix, box) per box
+        self.launches_per_step = 2 + 2 * launches  # sums, N2 table, (prefix, box) per box
         nb = sum(len(b) for b in self.stage_boxes)
         self.kernel_cmp_per_launch = p.n_f * (p.n_v * (p.n_v - 1) * (p.n_v - 2) // 6) / nb
 
