@@ -138,6 +138,8 @@ def run_local(problem, grid, balance: str = "split", keep_values: bool = True,
     acc = D.new_acc(dev)
     pieces = []
     count = 0
+    specs = []  # single-slab tasks without host streaming: batched into shared grids
+    tdt = D.torch_dtype(problem.precision)
     for p_r in range(grid.n_pr):
         for p_v in range(grid.n_pv):
             for ev in plan_2way(grid, RankCoords(0, p_v, p_r), n_vp, balance):
@@ -145,10 +147,21 @@ def run_local(problem, grid, balance: str = "split", keep_values: bool = True,
                     continue
                 rows = [blocks[p_f, ev.row_block] for p_f in range(grid.n_pf)]
                 cols = [blocks[p_f, ev.col_block] for p_f in range(grid.n_pf)]
-                piece = run_task(code, problem, grid, ev, rows, cols, sums[ev.row_block],
-                                 sums[ev.col_block], acc, keep_values, sink)
+                m, n = ev.r1 - ev.r0, ev.c1 - ev.c0
+                if grid.n_pf == 1 and sink is None:
+                    vals = torch.empty(D.pair_count(m, n, ev.diagonal), dtype=tdt,
+                                       device=dev) if keep_values else None
+                    W, V = rows[0], cols[0]
+                    specs.append((W, ev.r0, ev.r1, V, ev.c0, ev.c1, sums[ev.row_block],
+                                  sums[ev.col_block], ev.diagonal, vals))
+                    piece = PairPiece(W.v0 + ev.r0, V.v0 + ev.c0, m, n, ev.diagonal, 0, m, vals)
+                else:
+                    piece = run_task(code, problem, grid, ev, rows, cols, sums[ev.row_block],
+                                     sums[ev.col_block], acc, keep_values, sink)
                 pieces.append(piece)
                 count += D.pair_count(piece.m, piece.n, piece.diagonal)
+    for k in range(0, len(specs), 16):
+        D.czek2_tasks(code, specs[k:k + 16], problem.n_v, acc)
     end.record()
     end.synchronize()
     if sink is not None:
