@@ -8,12 +8,15 @@ Status codes map back onto the reference's exception families
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
 from .domain import ConfigError, DataError, EngineError
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libpsim.so"
+if os.environ.get("PSIM_LIB"):  # A/B experiments against another in-tree build
+    LIB_PATH = Path(os.environ["PSIM_LIB"]).resolve()
 
 F32, F64 = 0, 1
 
@@ -104,6 +107,8 @@ def lib() -> C.CDLL:
                     )
                 handle = C.CDLL(str(LIB_PATH))
                 for name, (res, args) in SIGNATURES.items():
+                    if os.environ.get("PSIM_LIB") and not hasattr(handle, name):
+                        continue  # an older build under A/B test
                     fn = getattr(handle, name)
                     fn.restype = res
                     fn.argtypes = args

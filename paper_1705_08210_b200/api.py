@@ -163,8 +163,12 @@ def run_2way(problem, grid, *, transport: str = "local", kernel: str | None = No
 def run_3way(problem, grid, *, stage: int | None = None, transport: str = "local",
              kernel: str | None = None, timeout: float = DEFAULT_TIMEOUT,
              inject_delay: float = 0.0, delay_seed: int = 0,
-             keep_values: bool = True) -> RunResult:
-    """All unique 3-way Czekanowski metrics of ``problem`` (or one stage)."""
+             keep_values: bool = True, host_values: bool = False) -> RunResult:
+    """All unique 3-way Czekanowski metrics of ``problem`` (or one stage).
+
+    ``host_values=True`` (local transport) streams each box's values to pinned
+    host memory in pivot-range chunks while the next chunk computes -- the
+    streaming form of the reference's result stages."""
     if problem.arity != 3:
         raise ConfigError(f"run_3way needs an arity-3 problem, got arity={problem.arity}")
     validate_grid(grid, problem.n_f, problem.n_v, 3)
@@ -180,5 +184,6 @@ def run_3way(problem, grid, *, stage: int | None = None, transport: str = "local
 
         out = dist.run_3way_nccl(problem, grid, stages, keep_values=keep_values)
     else:
-        out = engine3.run_local(problem, grid, stages, keep_values=keep_values)
+        out = engine3.run_local(problem, grid, stages, keep_values=keep_values,
+                                host_values=host_values)
     return _result(problem, grid, mode, out, None if stage is None else stages)

@@ -305,8 +305,27 @@ __host__ __device__ __forceinline__ int64_t first_col_tile(int64_t b, int64_t bm
 // bands of G ~ sqrt(resident CTAs); inside a band tiles run column-major (all
 // G rows of one column tile, then the next), so the CTAs resident at the same
 // time share ~G row panels and ~W/G column panels in L2 instead of one row
-// panel and W column panels (W = resident CTAs). In a diagonal band the tiles
-// left of a row's first column are enumerated too and exit at once -- at most
-// G(G-1)/2 empty CTAs per band.
+// panel and W column panels (W = resident CTAs). band_pref[b] = tiles before
+// band b (device); in a diagonal band the tiles left of a row's first column
+// are enumerated too and skipped (returns false) -- at most G(G-1)/2 empty
+// CTAs per band.
+__device__ __forceinline__ bool band_tile(int64_t t, const int64_t* __restrict__ band_pref,
+                                          int64_t nbands, int64_t G, int64_t row_tile0,
+                                          int64_t row_tile_end, int64_t bm, int64_t bn,
+                                          int diagonal, int& bi, int& bj) {
+  int64_t lo = 0, hi = nbands;
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (band_pref[mid] <= t) lo = mid; else hi = mid;
+  }
+  const int64_t r0 = row_tile0 + lo * G;
+  const int64_t rows = min64(G, row_tile_end - r0);
+  const int64_t u = t - band_pref[lo];
+  const int64_t b = r0 + u % rows;
+  const int64_t c = first_col_tile(r0, bm, bn, diagonal) + u / rows;
+  bi = (int)b;
+  bj = (int)c;
+  return c >= first_col_tile(b, bm, bn, diagonal);
+}
 
 }  // namespace psim

@@ -134,25 +134,57 @@ def run_boxes_field(code, problem, boxes, slab_blocks, sums, tables, acc, keep_v
     return count
 
 
-def run_boxes(code, problem, boxes, blocks, sums, tables, acc, keep_values, pieces) -> int:
+def pivot_chunks(box: Box, parts: int) -> list[Box]:
+    """Split a box along J into <= parts sub-boxes of about equal output."""
+    counts = []
+    for j in range(box.j0, box.j1):
+        r = max(0, min(box.i1, j) - box.i0)
+        c = max(0, box.k1 - max(box.k0, j + 1))
+        counts.append(r * c)
+    total = sum(counts)
+    if total == 0 or parts <= 1:
+        return [box]
+    out, start, run, k = [], box.j0, 0, 1
+    for jj, c in enumerate(counts):
+        run += c
+        if run >= total * k / parts and box.j0 + jj + 1 < box.j1:
+            out.append(Box(box.blocks, box.i0, box.i1, start, box.j0 + jj + 1, box.k0, box.k1))
+            start, k = box.j0 + jj + 1, k + 1
+    out.append(Box(box.blocks, box.i0, box.i1, start, box.j1, box.k0, box.k1))
+    return out
+
+
+def run_boxes(code, problem, boxes, blocks, sums, tables, acc, keep_values, pieces,
+              sink=None) -> int:
     count = 0
     tdt = D.torch_dtype(problem.precision)
     dev = acc.device
+    if sink is not None:  # pivot-range sub-boxes so each D2H overlaps the next launch
+        boxes = [sub for b in boxes for sub in pivot_chunks(b, sink.bands)]
     for box in boxes:
         probe = box_struct(box, blocks, sums, tables, problem.n_f, problem.n_v, None, acc)
         n_out, _ = box_plan(probe)
         if n_out == 0:
             continue
-        vals = torch.empty(n_out, dtype=tdt, device=dev) if keep_values else None
+        keep = keep_values or sink is not None
+        vals = torch.empty(n_out, dtype=tdt, device=dev) if keep else None
         b = box_struct(box, blocks, sums, tables, problem.n_f, problem.n_v, vals, acc)
         N.call("psim_czek3_box", code, C.byref(b), D.stream_ptr())
+        if sink is not None:
+            host = sink.buffer(n_out, tdt)
+            sink.copy(host, vals, 0, n_out)
+            vals = host
         pieces.append(BoxPiece(box.i0, box.i1, box.j0, box.j1, box.k0, box.k1, vals))
         count += n_out
     return count
 
 
-def run_local(problem, grid, stages, keep_values: bool = True) -> Outcome:
+def run_local(problem, grid, stages, keep_values: bool = True,
+              host_values: bool = False) -> Outcome:
+    from .engine2 import HostSink
+
     dev = torch.device("cuda", torch.cuda.current_device())
+    sink = HostSink() if host_values and grid.n_pf == 1 else None
     code = D.code_of(problem.precision)
     n_vp = problem.n_v // grid.n_pv
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -177,12 +209,14 @@ def run_local(problem, grid, stages, keep_values: bool = True) -> Outcome:
                     boxes.extend(unit_boxes(ev, n_vp, grid.n_st, stages))
             if grid.n_pf == 1:
                 count += run_boxes(code, problem, merge_boxes(boxes), blocks, sums, tables, acc,
-                                   keep_values, pieces)
+                                   keep_values, pieces, sink)
             else:
                 count += run_boxes_field(code, problem, merge_boxes(boxes), slab_blocks, sums,
                                          tables, acc, keep_values, pieces)
     end.record()
     end.synchronize()
+    if sink is not None:
+        sink.finish()
     lo, hi, deg = D.acc_words(acc)
     all_sums = torch.cat([sums[p] for p in range(grid.n_pv)]).cpu().numpy()
     return Outcome(pieces, lo, hi, deg, count, all_sums, start.elapsed_time(end) * 1e-3)

@@ -300,6 +300,18 @@ def test_band_launches_equal_single_launch():
     assert (a.records.values.view(np.uint64) == b.records.values.view(np.uint64)).all()
 
 
+def test_3way_streamed_host_values_equal_device_run():
+    """run_3way(host_values=True) splits boxes into pivot ranges and streams
+    them to pinned host memory; results must equal the plain run."""
+    P = _api()
+    prob = P.Problem(3, 500, 96, P.gen_uniform(12, 500, 96), "single")
+    for grid in (P.DecompGrid(), P.DecompGrid(n_pv=2, n_st=2)):
+        a = P.run_3way(prob, grid)
+        b = P.run_3way(prob, grid, host_values=True)
+        assert a.checksum == b.checksum
+        assert (a.records.values.view(np.uint32) == b.records.values.view(np.uint32)).all()
+
+
 def test_data_errors_on_device():
     P = _api()
     m = np.ones((4, 4))
