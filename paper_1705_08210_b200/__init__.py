@@ -29,6 +29,7 @@ from .domain import (  # noqa: F401
     unique_tuple_count,
 )
 from .plan import owns_pair, owns_triple, plan_2way, plan_3way, stage_range  # noqa: F401
+from .vectorfile import VectorFileSpec, write_vectors  # noqa: F401
 from .synthetic import (  # noqa: F401
     Checksum128,
     SyntheticSpec,

@@ -95,6 +95,12 @@ def load_block(problem, grid, coords, device, pinned_cache: dict | None = None) 
             N.call("psim_gen_uniform", code, src.seed, src.n_v, f0, v0, n_fp, n_vp, ptr(data),
                    ld, st)
         return Block(data, n_fp, n_vp, ld, v0, problem.precision)
+    from .vectorfile import is_vector_file, stream_to_device
+
+    if is_vector_file(src) and src.precision == problem.precision:
+        stream_to_device(src, problem, grid, coords, data)  # file -> pinned chunks -> HBM
+        check_values(data, n_fp, n_vp, ld, code)
+        return Block(data, n_fp, n_vp, ld, v0, problem.precision)
     arr = host_block(problem, grid, coords)  # (n_fp, n_vp) Fortran
     host = torch.from_numpy(np.ascontiguousarray(arr.T))  # (n_vp, n_fp) == same bytes
     data[:, :n_fp].copy_(host, non_blocking=host.is_pinned())

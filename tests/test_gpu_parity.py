@@ -312,6 +312,44 @@ def test_3way_streamed_host_values_equal_device_run():
         assert (a.records.values.view(np.uint32) == b.records.values.view(np.uint32)).all()
 
 
+def test_vector_file_input_streams_to_device(tmp_path):
+    """f4: runs fed from a raw vector file (streamed through pinned chunks into
+    HBM) equal runs on the same data generated in HBM, for vector and field
+    slabs; bad files raise DataError like the reference (io.py:78-117)."""
+    from oracle import propsim_np as O
+    from paper_1705_08210_b200 import vectorfile
+
+    P = _api()
+    n_f, n_v = 640, 96
+    for precision, dt in (("double", np.float64), ("single", np.float32)):
+        V = O.uniform(17, n_f, n_v, dt)
+        spec = P.write_vectors(tmp_path / f"v_{precision}.bin", V, precision)
+        old = vectorfile.CHUNK_BYTES
+        vectorfile.CHUNK_BYTES = n_f * 8 * 7  # several chunks per slab
+        try:
+            for grid in (P.DecompGrid(), P.DecompGrid(n_pv=3), P.DecompGrid(n_pf=2, n_pv=2)):
+                a = P.run_2way(P.Problem(2, n_f, n_v, spec, precision), grid)
+                b = P.run_2way(P.Problem(2, n_f, n_v, P.gen_uniform(17, n_f, n_v), precision),
+                               grid)
+                assert a.checksum == b.checksum, (precision, grid)
+            r3 = P.run_3way(P.Problem(3, n_f, n_v, spec, precision), P.DecompGrid(n_pv=2))
+            w3 = P.run_3way(P.Problem(3, n_f, n_v, P.gen_uniform(17, n_f, n_v), precision),
+                            P.DecompGrid(n_pv=2))
+            assert r3.checksum == w3.checksum
+        finally:
+            vectorfile.CHUNK_BYTES = old
+    bad = tmp_path / "short.bin"
+    bad.write_bytes(b"\0" * 100)
+    with pytest.raises(P.DataError):
+        P.run_2way(P.Problem(2, n_f, n_v, P.VectorFileSpec(str(bad), n_f, n_v)), P.DecompGrid())
+    nan = np.ones((n_f, n_v))
+    nan[5, 7] = np.nan
+    nan.ravel(order="F").tofile(tmp_path / "nan.bin")
+    with pytest.raises(P.DataError):
+        P.run_2way(P.Problem(2, n_f, n_v, P.VectorFileSpec(str(tmp_path / "nan.bin"), n_f, n_v)),
+                   P.DecompGrid())
+
+
 def test_data_errors_on_device():
     P = _api()
     m = np.ones((4, 4))

@@ -165,6 +165,24 @@ def test_exactness_guard_and_generator_kat():
     assert blk.tolist() == [[1570, 202, 805], [1317, 331, 1052], [759, 1667, 60], [702, 1349, 199]]
 
 
+def test_vector_file_format_and_slices(tmp_path):
+    """Headerless little-endian column-major files (reference io.py:1-14, 89-117)."""
+    rng = np.random.default_rng(1)
+    M = rng.random((12, 10))
+    spec = P.write_vectors(tmp_path / "m.bin", M)
+    assert (tmp_path / "m.bin").read_bytes() == M.astype("<f8").ravel(order="F").tobytes()
+    assert spec.expected_nbytes == 12 * 10 * 8
+    prob = P.Problem(2, 12, 10, spec)
+    g = P.DecompGrid(n_pf=2, n_pv=5)
+    blk = spec.local_block(prob, g, RankCoords(1, 3, 0))
+    assert (blk == M[6:12, 6:8]).all() and blk.flags.f_contiguous
+    with pytest.raises(P.DataError):
+        P.write_vectors(tmp_path / "neg.bin", -M)
+    (tmp_path / "short.bin").write_bytes(b"\0" * 8)
+    with pytest.raises(P.DataError):
+        P.VectorFileSpec(str(tmp_path / "short.bin"), 12, 10).check_size()
+
+
 def test_checksum_host_utility_kat():
     recs = [P.MetricRecord(P.TupleId(ix), np.float64(v))
             for ix, v in [((0, 1), 0.8), ((0, 2), 2.0 / 3.0), ((1, 2), 0.75)]]
