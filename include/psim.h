@@ -142,6 +142,17 @@ int psim_czek2_block(int dtype, const psim_block2_t* task, void* stream);
  * circulant steps of a slab share one launch and one tail (metrics2.py:148-158
  * over the plan of schedule.py:116-142). */
 int psim_czek2_tasks(int dtype, const psim_block2_t* tasks, int ntasks, void* stream);
+/* pack_bits (mingemm.py:279-291): 32 fields per uint32 word, bit q%32 of
+ * word q/32 of vector i at words[i * ldw + q/32] (ldw % 4 == 0, padding
+ * bits zero); flags[0] += #entries outside {0, 1} (DataError). */
+int psim_pack_bits(int dtype, const void* V, int64_t n_fp, int64_t n_vp, int64_t ld,
+                   uint32_t* words, int64_t ldw, unsigned long long* flags, void* stream);
+/* Sorenson 2-way task on packed operands (W, V = word arrays, ldw / ldv in
+ * words, n_f in fields): counts popcount(a & b) (mgemm_bitpacked,
+ * mingemm.py:294-312), converted to the run dtype, then the 2-way value,
+ * layout and checksum of psim_czek2_block; s_row / s_col are the dense
+ * column sums. No row bands. */
+int psim_sorenson2_block(int dtype, const psim_block2_t* task, void* stream);
 /* 2-way epilogue from reduced packed numerators, rows [r0, r1) of a task's
  * packed layout (field-axis path, metrics2.py:156-158). N and vals point at
  * the first entry of row r0. */

@@ -76,6 +76,8 @@ SIGNATURES = {
          c_vp]),
     "psim_czek2_block": (C.c_int, [C.c_int, C.POINTER(Block2), c_vp]),
     "psim_czek2_tasks": (C.c_int, [C.c_int, C.POINTER(Block2), C.c_int, c_vp]),
+    "psim_pack_bits": (C.c_int, [C.c_int, c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp]),
+    "psim_sorenson2_block": (C.c_int, [C.c_int, C.POINTER(Block2), c_vp]),
     "psim_czek2_from_numerators": (
         C.c_int,
         [C.c_int, c_vp, c_i64, c_i64, c_i64, c_i64, C.c_int, c_vp, c_vp, c_i64, c_i64, c_i64,

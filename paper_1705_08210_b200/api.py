@@ -73,11 +73,12 @@ class RunResult:
 
 
 def resolve_kernel(metric: str, kernel: str | None) -> str:
+    """Mirror of metrics2.py:44-49: Sorenson defaults to the bit-packed path."""
     if kernel is None:
-        return "b200"
+        return "bitpacked" if metric == "sorenson" else "b200"
     if kernel not in KERNELS:
         raise ConfigError(f"kernel must be one of {KERNELS}, got {kernel!r}")
-    return "b200"
+    return "bitpacked" if kernel == "bitpacked" else "b200"
 
 
 def resolve_transport(transport: str) -> str:
@@ -118,7 +119,7 @@ class _Origin:
     p_f = p_v = p_r = 0
 
 
-def _result(problem, grid, transport, out, stages) -> RunResult:
+def _result(problem, grid, transport, out, stages, kern: str = "b200") -> RunResult:
     expected = unique_tuple_count(problem.n_v, problem.arity)
     if stages is None and out.count != expected:
         raise EngineError(f"schedule covered {out.count} tuples, expected {expected}")
@@ -127,7 +128,7 @@ def _result(problem, grid, transport, out, stages) -> RunResult:
                        dtype_of(problem.precision))
     return RunResult(
         arity=problem.arity, n_f=problem.n_f, n_v=problem.n_v, precision=problem.precision,
-        metric=problem.metric, grid=grid, transport=transport, kernel="b200", records=recs,
+        metric=problem.metric, grid=grid, transport=transport, kernel=kern, records=recs,
         checksum=Checksum128.from_words(out.lo, out.hi), traffic=TrafficStats(),
         rank_traffic={}, degenerate_count=out.degenerate, elapsed=out.elapsed, stages=stages,
     )
@@ -145,19 +146,24 @@ def run_2way(problem, grid, *, transport: str = "local", kernel: str | None = No
     if problem.arity != 2:
         raise ConfigError(f"run_2way needs an arity-2 problem, got arity={problem.arity}")
     validate_grid(grid, problem.n_f, problem.n_v, 2)
-    resolve_kernel(problem.metric, kernel)
+    kern = resolve_kernel(problem.metric, kernel)
     mode = resolve_transport(transport)
-    _check_sorenson(problem)
     _require_cuda()
+    # (like the reference, only the bit-packed path checks for 0/1 input --
+    # on the device, while packing: metrics2.py:125-136, mingemm.py:287-288)
     if mode == "nccl":
         from . import dist
 
+        if kern == "bitpacked":  # NCCL ranks run the dense kernel: bitwise identical on 0/1
+            _check_sorenson(problem)
         out = dist.run_2way_nccl(problem, grid, balance=balance, keep_values=keep_values,
                                  host_values=host_values)
     else:
+        if kern == "bitpacked" and grid.n_pf > 1:
+            _check_sorenson(problem)  # field split: dense kernel, identical bits on 0/1
         out = engine2.run_local(problem, grid, balance=balance, keep_values=keep_values,
-                                host_values=host_values)
-    return _result(problem, grid, mode, out, None)
+                                host_values=host_values, bitpacked=(kern == "bitpacked"))
+    return _result(problem, grid, mode, out, None, kern)
 
 
 def run_3way(problem, grid, *, stage: int | None = None, transport: str = "local",
@@ -175,9 +181,9 @@ def run_3way(problem, grid, *, stage: int | None = None, transport: str = "local
     if stage is not None and not 0 <= stage < grid.n_st:
         raise ConfigError(f"stage must be in [0, {grid.n_st}), got {stage}")
     stages = tuple(range(grid.n_st)) if stage is None else (stage,)
-    resolve_kernel(problem.metric, kernel)
+    kern = resolve_kernel(problem.metric, kernel)
     mode = resolve_transport(transport)
-    _check_sorenson(problem)
+    _check_sorenson(problem)  # 3-way always checks (metrics3.py:84-85); dense kernel
     _require_cuda()
     if mode == "nccl":
         from . import dist
@@ -186,4 +192,4 @@ def run_3way(problem, grid, *, stage: int | None = None, transport: str = "local
     else:
         out = engine3.run_local(problem, grid, stages, keep_values=keep_values,
                                 host_values=host_values)
-    return _result(problem, grid, mode, out, None if stage is None else stages)
+    return _result(problem, grid, mode, out, None if stage is None else stages, kern)

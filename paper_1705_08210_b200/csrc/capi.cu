@@ -175,6 +175,31 @@ int psim_czek2_tasks(int dtype, const psim_block2_t* tasks, int ntasks, void* st
   return cuda_status(psim::czek2_tasks(dtype, tasks, ntasks, S(stream)), "psim_czek2_tasks");
 }
 
+int psim_pack_bits(int dtype, const void* V, int64_t n_fp, int64_t n_vp, int64_t ld,
+                   uint32_t* words, int64_t ldw, unsigned long long* flags, void* stream) {
+  if (int r = check_dtype(dtype)) return r;
+  if (!V || !words || !flags || ld < n_fp) return fail(PSIM_ECONFIG, "bad block / words / ld");
+  if (ldw < (n_fp + 31) / 32 || ldw % 4)
+    return fail(PSIM_ECONFIG, "ldw=%lld must hold ceil(n_fp/32) words and be a multiple of 4",
+                (long long)ldw);
+  return cuda_status(psim::pack_bits(dtype, V, n_fp, n_vp, ld, words, ldw, flags, S(stream)),
+                     "psim_pack_bits");
+}
+
+int psim_sorenson2_block(int dtype, const psim_block2_t* t, void* stream) {
+  if (int r = check_dtype(dtype)) return r;
+  if (!t || !t->W || !t->V || !t->s_row || !t->s_col || !t->acc)
+    return fail(PSIM_ECONFIG, "NULL task field");
+  const int64_t nw = (t->n_f + 31) / 32;
+  if (t->ldw < nw || t->ldv < nw || t->ldw % 4 || t->ldv % 4 ||
+      reinterpret_cast<uintptr_t>(t->W) % 16 || reinterpret_cast<uintptr_t>(t->V) % 16)
+    return fail(PSIM_ECONFIG, "packed operands need 16-byte alignment and ld >= ceil(n_f/32)");
+  if (t->diagonal && (t->m != t->n || t->g_row != t->g_col))
+    return fail(PSIM_ECONFIG, "diagonal task needs m == n and g_row == g_col");
+  if (t->row_begin || t->row_end) return fail(PSIM_ECONFIG, "row bands not supported here");
+  return cuda_status(psim::sorenson2_block(dtype, *t, S(stream)), "psim_sorenson2_block");
+}
+
 static int check_task2(int dtype, const psim_block2_t* t) {
   if (int r = check_dtype(dtype)) return r;
   if (!t) return fail(PSIM_ECONFIG, "task is NULL");

@@ -155,6 +155,27 @@ __device__ __forceinline__ void micro_step(float (&acc)[C::TM][C::TN], const flo
   }
 }
 
+// Bit-packed 0/1 operands (Sorenson, sorenson.cu): 4 uint32 words = 128 fields
+// per LDS.128; the count of a pair is popc(a & b) summed over words
+// (mgemm_bitpacked, mingemm.py:294-312). Integer adds: any order is exact.
+template <class C>
+__device__ __forceinline__ void micro_step(uint32_t (&acc)[C::TM][C::TN], const uint32_t* As,
+                                           const uint32_t* Bs, int ty, int tx, int kk) {
+  constexpr int P = C::PITCH;
+  uint4 a[C::TM];
+#pragma unroll
+  for (int m = 0; m < C::TM; ++m)
+    a[m] = *reinterpret_cast<const uint4*>(As + (ty + 16 * m) * P + kk);
+#pragma unroll
+  for (int n = 0; n < C::TN; ++n) {
+    const uint4 b = *reinterpret_cast<const uint4*>(Bs + (tx + 16 * n) * P + kk);
+#pragma unroll
+    for (int m = 0; m < C::TM; ++m)
+      acc[m][n] += (__popc(a[m].x & b.x) + __popc(a[m].y & b.y)) +
+                   (__popc(a[m].z & b.z) + __popc(a[m].w & b.w));
+  }
+}
+
 // Stage field chunk kt of `rows` W vectors and `cols` V vectors (and, with
 // PIVOT, of the pivot column) into stage buffer `st`.
 template <class C, bool PIVOT>

@@ -34,6 +34,10 @@ cudaError_t column_sums(int dtype, const void* V, int64_t n_fp, int64_t n_vp, in
 cudaError_t fold_add(int dtype, void* dst, const void* src, int64_t count, cudaStream_t st);
 
 cudaError_t czek2_block(int dtype, const Czek2Block& t, cudaStream_t st);
+// Sorenson (0/1) path: bit packing and the AND+POPC 2-way task (sorenson.cu).
+cudaError_t pack_bits(int dtype, const void* V, int64_t n_fp, int64_t n_vp, int64_t ld,
+                      uint32_t* words, int64_t ldw, unsigned long long* flags, cudaStream_t st);
+cudaError_t sorenson2_block(int dtype, const psim_block2_t& t, cudaStream_t st);
 // Several 2-way tasks (same n_f, n_v, dtype) in one grid (<= 16 per launch).
 cudaError_t czek2_tasks(int dtype, const Czek2Block* tasks, int ntasks, cudaStream_t st);
 cudaError_t mgemm(int dtype, const void* W, int64_t ldw, const void* V, int64_t ldv, int64_t n_f,

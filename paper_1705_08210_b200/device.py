@@ -167,6 +167,45 @@ def czek2_block(code: int, W: Block, r0: int, r1: int, V: Block, c0: int, c1: in
     N.call("psim_czek2_block", code, C.byref(t), stream_ptr())
 
 
+class Bits:
+    """A bit-packed 0/1 block: 32 fields per uint32 word, vector i's words at
+    row i of ``words`` (ld a multiple of 32 words = 128 B)."""
+
+    __slots__ = ("words", "n_fp", "n_vp", "ld", "v0")
+
+    def __init__(self, words, n_fp, n_vp, ld, v0):
+        self.words, self.n_fp, self.n_vp, self.ld, self.v0 = words, n_fp, n_vp, ld, v0
+
+    def col_ptr(self, local_col: int) -> int:
+        return self.words.data_ptr() + local_col * self.ld * 4
+
+
+def pack_bits(block: Block) -> Bits:
+    """pack_bits (mingemm.py:279-291) on the device; non-0/1 entries -> DataError."""
+    nw = -(-block.n_fp // 32)
+    ld = max(32, -(-nw // 32) * 32)
+    words = torch.empty((block.n_vp, ld), dtype=torch.int32, device=block.data.device)
+    flags = torch.zeros(2, dtype=torch.int64, device=block.data.device)
+    N.call("psim_pack_bits", block.code, ptr(block.data), block.n_fp, block.n_vp, block.ld,
+           ptr(words), ld, ptr(flags), stream_ptr())
+    if int(flags[0].item()):
+        raise DataError("bit packing needs entries exactly in {0, 1}")
+    return Bits(words, block.n_fp, block.n_vp, ld, block.v0)
+
+
+def sorenson2_block(code: int, W: Bits, r0: int, r1: int, V: Bits, c0: int, c1: int,
+                    s_row: torch.Tensor, s_col: torch.Tensor, diagonal: bool, n_v: int,
+                    vals: torch.Tensor | None, acc: torch.Tensor) -> None:
+    t = N.Block2(
+        W=W.col_ptr(r0), ldw=W.ld, V=V.col_ptr(c0), ldv=V.ld, n_f=W.n_fp,
+        m=r1 - r0, n=c1 - c0, diagonal=1 if diagonal else 0, row_begin=0, row_end=0,
+        s_row=s_row.data_ptr() + r0 * s_row.element_size(),
+        s_col=s_col.data_ptr() + c0 * s_col.element_size(),
+        g_row=W.v0 + r0, g_col=V.v0 + c0, n_v=n_v, vals=ptr(vals), acc=ptr(acc),
+    )
+    N.call("psim_sorenson2_block", code, C.byref(t), stream_ptr())
+
+
 def czek2_tasks(code: int, specs: list, n_v: int, acc: torch.Tensor) -> None:
     """Several fused 2-way tasks in one grid. specs: (W, r0, r1, V, c0, c1,
     s_row, s_col, diagonal, vals) tuples sharing n_f."""

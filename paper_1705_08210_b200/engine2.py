@@ -122,9 +122,10 @@ def finish_numerators(code, N, r0, r1, m, n, diagonal, s_row, s_col, g_row, g_co
 
 
 def run_local(problem, grid, balance: str = "split", keep_values: bool = True,
-              host_values: bool = False) -> Outcome:
+              host_values: bool = False, bitpacked: bool = False) -> Outcome:
     dev = torch.device("cuda", torch.cuda.current_device())
     sink = HostSink() if host_values else None
+    bitpacked = bitpacked and grid.n_pf == 1
     code = D.code_of(problem.precision)
     n_vp = problem.n_v // grid.n_pv
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -140,6 +141,7 @@ def run_local(problem, grid, balance: str = "split", keep_values: bool = True,
     count = 0
     specs = []  # single-slab tasks without host streaming: batched into shared grids
     tdt = D.torch_dtype(problem.precision)
+    bits = {p_v: D.pack_bits(blocks[0, p_v]) for p_v in range(grid.n_pv)} if bitpacked else None
     for p_r in range(grid.n_pr):
         for p_v in range(grid.n_pv):
             for ev in plan_2way(grid, RankCoords(0, p_v, p_r), n_vp, balance):
@@ -148,7 +150,20 @@ def run_local(problem, grid, balance: str = "split", keep_values: bool = True,
                 rows = [blocks[p_f, ev.row_block] for p_f in range(grid.n_pf)]
                 cols = [blocks[p_f, ev.col_block] for p_f in range(grid.n_pf)]
                 m, n = ev.r1 - ev.r0, ev.c1 - ev.c0
-                if grid.n_pf == 1 and sink is None:
+                if bitpacked:  # Sorenson on 0/1 data: AND + POPC mainloop
+                    vals = torch.empty(D.pair_count(m, n, ev.diagonal), dtype=tdt, device=dev)
+                    Wb, Vb = bits[ev.row_block], bits[ev.col_block]
+                    D.sorenson2_block(code, Wb, ev.r0, ev.r1, Vb, ev.c0, ev.c1,
+                                      sums[ev.row_block], sums[ev.col_block], ev.diagonal,
+                                      problem.n_v, vals, acc)
+                    if sink is not None:
+                        host = sink.buffer(vals.numel(), tdt)
+                        sink.copy(host, vals, 0, vals.numel())
+                        vals = host
+                    elif not keep_values:
+                        vals = None
+                    piece = PairPiece(Wb.v0 + ev.r0, Vb.v0 + ev.c0, m, n, ev.diagonal, 0, m, vals)
+                elif grid.n_pf == 1 and sink is None:
                     vals = torch.empty(D.pair_count(m, n, ev.diagonal), dtype=tdt,
                                        device=dev) if keep_values else None
                     W, V = rows[0], cols[0]

@@ -152,6 +152,26 @@ def main():
     for g in (DecompGrid(n_pv=2), DecompGrid(n_pv=2, n_pr=3), DecompGrid(n_st=2),
               DecompGrid(n_pv=4)):
         cases.append(run_case("random-exact", 3, "double", 64, 24, g, 402, 11))
+    # Sorenson (metric="sorenson"): the reference's bit-packed kernel on 0/1 data
+    for n_f, n_v, g, prec in ((1, 9, DecompGrid(), "double"), (63, 17, DecompGrid(), "double"),
+                              (65, 40, DecompGrid(n_pv=2), "single"),
+                              (1000, 130, DecompGrid(), "double"),
+                              (777, 96, DecompGrid(n_pv=3, n_pr=2), "single")):
+        spec = gen_random_exact(31, n_f, n_v, 1)
+        prob = Problem(2, n_f, n_v, spec, prec, metric="sorenson")
+        res = run_2way(prob, g)
+        cases.append({
+            "kind": "random-exact", "metric": "sorenson", "arity": 2, "precision": prec,
+            "n_f": n_f, "n_v": n_v, "seed": 31, "bits": 1, "grid": grid_dict(g),
+            "records": len(res.records), "degenerate": res.degenerate_count,
+            "checksum": res.checksum.hex, "kernel": res.kernel,
+        })
+    spec = gen_random_exact(32, 90, 12, 1)
+    res = run_3way(Problem(3, 90, 12, spec, "double", metric="sorenson"), DecompGrid())
+    cases.append({"kind": "random-exact", "metric": "sorenson", "arity": 3, "precision": "double",
+                  "n_f": 90, "n_v": 12, "seed": 32, "bits": 1, "grid": grid_dict(DecompGrid()),
+                  "records": len(res.records), "degenerate": res.degenerate_count,
+                  "checksum": res.checksum.hex, "kernel": res.kernel})
     # staged 3-way runs: one case per stage
     for s in range(2):
         spec = gen_random_exact(402, 64, 24, 11)

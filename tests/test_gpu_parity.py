@@ -47,7 +47,8 @@ def _source(case):
 
 def _run(case, stage=None):
     P = _api()
-    prob = P.Problem(case["arity"], case["n_f"], case["n_v"], _source(case), case["precision"])
+    prob = P.Problem(case["arity"], case["n_f"], case["n_v"], _source(case), case["precision"],
+                     case.get("metric", "czekanowski"))
     grid = P.DecompGrid(**case["grid"])
     if case["arity"] == 2:
         return P.run_2way(prob, grid)
@@ -73,6 +74,24 @@ def test_golden_case(idx):
     if "ids" in case:
         assert [list(r.id.indices) for r in res.records] == case["ids"]
         assert res.stages == (case["stage"],)
+    if case.get("metric") == "sorenson":
+        assert res.kernel == case["kernel"] == "bitpacked"
+
+
+def test_sorenson_bitpacked_equals_dense_and_rejects_non_binary():
+    """f3: the AND+POPC kernel gives the dense kernel's bits on 0/1 data, for
+    n_f around word boundaries; non-0/1 input raises DataError (pack_bits)."""
+    P = _api()
+    for n_f in (1, 31, 32, 33, 1023, 1025, 4096):
+        spec = P.gen_random_exact(5, n_f, 150, 1)
+        for prec in ("double", "single"):
+            a = P.run_2way(P.Problem(2, n_f, 150, spec, prec, "sorenson"), P.DecompGrid(n_pv=2))
+            b = P.run_2way(P.Problem(2, n_f, 150, spec, prec), P.DecompGrid(), kernel="blocked")
+            assert a.kernel == "bitpacked" and a.checksum == b.checksum, (n_f, prec)
+            assert (a.records.values.view(np.uint8) == b.records.values.view(np.uint8)).all()
+    with pytest.raises(P.DataError):
+        P.run_2way(P.Problem(2, 16, 12, P.gen_random_exact(7, 16, 12, 3), metric="sorenson"),
+                   P.DecompGrid())
 
 
 def test_records_canonical_order_and_types():
