@@ -218,11 +218,20 @@ class Resident2:
         b = self.block
         s = D.column_sums(b)
         self.acc.zero_()
+        sor = self.problem.metric == "sorenson"
+        if sor:  # f3: pack 0/1 fields into words, then the AND+POPC kernel
+            self.kernel_name = "k_sorenson2<T> (psim_sorenson2_block)"
+            self.launches_per_step = 4  # sums, pack, band prefix, kernel
+            bits = D.pack_bits(b)
         if timed:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-        D.czek2_block(self.code, b, 0, b.n_vp, b, 0, b.n_vp, s, s, True, self.problem.n_v,
-                      self.vals, self.acc)
+        if sor:
+            D.sorenson2_block(self.code, bits, 0, b.n_vp, bits, 0, b.n_vp, s, s, True,
+                              self.problem.n_v, self.vals, self.acc)
+        else:
+            D.czek2_block(self.code, b, 0, b.n_vp, b, 0, b.n_vp, s, s, True, self.problem.n_v,
+                          self.vals, self.acc)
         if timed:
             e1.record()
             return [(e0, e1)]
