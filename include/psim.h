@@ -163,6 +163,11 @@ int psim_czek2_from_numerators(int dtype, const void* N, int64_t r0, int64_t r1,
 /* One step of the ordered field-axis fold (RankContext.reduce_field_axis,
  * engine.py:197-216): dst[e] = dst[e] + src[e]. */
 int psim_fold_add(int dtype, void* dst, const void* src, int64_t count, void* stream);
+/* Byte output mode (io.py:122-136, write_metrics 'byte'): out[e] =
+ * floor(clamp(vals[e], 0, 1) * 255 + 0.5) evaluated in double; *flag |= 1 when
+ * any value is non-finite (the caller raises DataError, like quantize_values). */
+int psim_quantize_bytes(int dtype, const void* vals, int64_t count, uint8_t* out,
+                        unsigned long long* flag, void* stream);
 /* Output element count and CTA-tile count of a 3-way box (host-only, sync). */
 int psim_box3_plan(int dtype, const psim_box3_t* box, int64_t* n_out, int64_t* n_tiles);
 /* Fused 3-way box (see psim_box3_t). */

@@ -41,3 +41,15 @@ from .synthetic import (  # noqa: F401
     mix64,
     value_bits,
 )
+from .output import (  # noqa: F401
+    MetricOutputSpec,
+    dequantize_byte,
+    owned_tuples,
+    quantize_byte,
+    read_metrics,
+    read_run_output,
+    read_run_values,
+    reconstruct_index,
+    write_metrics,
+    write_run_output,
+)

@@ -238,6 +238,15 @@ int psim_fold_add(int dtype, void* dst, const void* src, int64_t count, void* st
   return cuda_status(psim::fold_add(dtype, dst, src, count, S(stream)), "psim_fold_add");
 }
 
+int psim_quantize_bytes(int dtype, const void* vals, int64_t count, uint8_t* out,
+                        unsigned long long* flag, void* stream) {
+  if (int r = check_dtype(dtype)) return r;
+  if (count < 0) return fail(PSIM_ECONFIG, "count must be >= 0");
+  if (count > 0 && (!vals || !out || !flag)) return fail(PSIM_ECONFIG, "NULL argument");
+  return cuda_status(psim::quantize_bytes(dtype, vals, count, out, flag, S(stream)),
+                     "psim_quantize_bytes");
+}
+
 int psim_box3_plan(int dtype, const psim_box3_t* box, int64_t* n_out, int64_t* n_tiles) {
   if (int r = check_dtype(dtype)) return r;
   if (!box) return fail(PSIM_ECONFIG, "box is NULL");

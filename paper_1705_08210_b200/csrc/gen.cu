@@ -167,4 +167,72 @@ cudaError_t fold_add(int dtype, void* dst, const void* src, int64_t count, cudaS
   return cudaGetLastError();
 }
 
+// Byte output mode (io.py:122-136): floor(clamp(v, 0, 1) * 255 + 0.5) in
+// double, the multiply and add rounded separately (no FMA contraction) so the
+// byte equals numpy's. Eight values per thread: one 8-byte store.
+__device__ __forceinline__ uint32_t quant1(double v, int& bad) {
+  bad |= !isfinite(v);
+  const double c = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+  return (uint32_t)floor(__dadd_rn(__dmul_rn(c, 255.0), 0.5));
+}
+
+template <typename T>
+__global__ void k_quantize(const T* __restrict__ vals, int64_t count, uint8_t* __restrict__ out,
+                           unsigned long long* __restrict__ flag, int vec) {
+  int bad = 0;
+  const int64_t groups = count / 8;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < groups; g += stride) {
+    double v[8];
+    if (vec && sizeof(T) == 8) {
+      const double2* p = reinterpret_cast<const double2*>(vals + g * 8);
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const double2 x = __ldcs(p + h);
+        v[2 * h] = x.x;
+        v[2 * h + 1] = x.y;
+      }
+    } else if (vec) {
+      const float4* p = reinterpret_cast<const float4*>(vals + g * 8);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float4 x = __ldcs(p + h);
+        v[4 * h] = x.x; v[4 * h + 1] = x.y; v[4 * h + 2] = x.z; v[4 * h + 3] = x.w;
+      }
+    } else {
+#pragma unroll
+      for (int h = 0; h < 8; ++h) v[h] = (double)vals[g * 8 + h];
+    }
+    uint32_t lo = 0, hi = 0;
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      lo |= quant1(v[h], bad) << (8 * h);
+      hi |= quant1(v[4 + h], bad) << (8 * h);
+    }
+    if (vec)
+      reinterpret_cast<uint2*>(out)[g] = make_uint2(lo, hi);
+    else
+      for (int h = 0; h < 8; ++h) out[g * 8 + h] = (uint8_t)(((h < 4 ? lo : hi) >> (8 * (h & 3))) & 255u);
+  }
+  const int64_t tail = groups * 8 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (tail < count && tail < groups * 8 + 8) out[tail] = (uint8_t)quant1((double)vals[tail], bad);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1ull);
+}
+
+cudaError_t quantize_bytes(int dtype, const void* vals, int64_t count, void* out, void* flag,
+                           cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  const unsigned g = grid_for((count + 7) / 8, 256);
+  const uintptr_t a = reinterpret_cast<uintptr_t>(vals), b = reinterpret_cast<uintptr_t>(out);
+  const int vec = (a % 16 == 0) && (b % 8 == 0);
+  auto* f = static_cast<unsigned long long*>(flag);
+  if (dtype == kF64)
+    k_quantize<double><<<g, 256, 0, st>>>(static_cast<const double*>(vals), count,
+                                          static_cast<uint8_t*>(out), f, vec);
+  else
+    k_quantize<float><<<g, 256, 0, st>>>(static_cast<const float*>(vals), count,
+                                         static_cast<uint8_t*>(out), f, vec);
+  return cudaGetLastError();
+}
+
 }  // namespace psim

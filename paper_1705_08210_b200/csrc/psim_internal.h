@@ -32,6 +32,8 @@ cudaError_t check_block(int dtype, const void* V, int64_t n_fp, int64_t n_vp, in
 cudaError_t column_sums(int dtype, const void* V, int64_t n_fp, int64_t n_vp, int64_t ld,
                         void* out, cudaStream_t st);
 cudaError_t fold_add(int dtype, void* dst, const void* src, int64_t count, cudaStream_t st);
+cudaError_t quantize_bytes(int dtype, const void* vals, int64_t count, void* out, void* flag,
+                           cudaStream_t st);
 
 cudaError_t czek2_block(int dtype, const Czek2Block& t, cudaStream_t st);
 // Sorenson (0/1) path: bit packing and the AND+POPC 2-way task (sorenson.cu).

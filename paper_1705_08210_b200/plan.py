@@ -98,8 +98,10 @@ def tasks_2way(grid, n_vp: int, balance: str = "split") -> dict[int, tuple[Task2
     return out
 
 
-def owns_pair(i: int, j: int, n_v: int, grid, balance: str = "split") -> tuple[int, int]:
-    """(rank with p_f = 0, task position) computing canonical pair (i, j)."""
+def owns_pair(i: int, j: int, n_v: int, grid, balance: str = "reference") -> tuple[int, int]:
+    """(rank with p_f = 0, task position) computing canonical pair (i, j) under
+    the given plan balance; the default is the reference's owner
+    (schedule.py:154-177), the one output files are laid out by."""
     if not 0 <= i < j < n_v:
         raise ValueError(f"need 0 <= i < j < n_v, got ({i}, {j})")
     if n_v % grid.n_pv:

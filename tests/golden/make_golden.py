@@ -184,8 +184,71 @@ def main():
             "checksum": res.checksum.hex,
             "ids": [list(r.id.indices) for r in res.records],
         })
-    OUT.write_text(json.dumps({"kat": kat, "cases": cases}, indent=0))
+    OUT.write_text(json.dumps({"kat": kat, "cases": cases, "outputs": output_cases(),
+                               "owners": owner_tables()}, indent=0))
     print(f"wrote {OUT} ({len(cases)} cases)")
+
+
+def owner_tables():
+    """Reference owns_pair / owns_triple for every tuple of small grids."""
+    from propsim.schedule import owns_pair, owns_triple
+    from propsim.core import iter_pairs, iter_triples
+
+    out = []
+    for n_v, g in ((24, DecompGrid(n_pv=3, n_pr=2)), (24, DecompGrid(n_pv=4, n_pr=3, n_pf=2)),
+                   (30, DecompGrid(n_pv=5, n_pr=4)), (12, DecompGrid(n_pv=6))):
+        out.append({"arity": 2, "n_v": n_v, "grid": grid_dict(g),
+                    "rank": [owns_pair(i, j, n_v, g)[0] for i, j in iter_pairs(n_v)]})
+    for n_v, g in ((24, DecompGrid(n_pv=2, n_pr=3)), (36, DecompGrid(n_pv=3, n_pr=5, n_st=2)),
+                   (48, DecompGrid(n_pv=4, n_pr=7, n_pf=2)), (24, DecompGrid(n_st=2, n_pr=2))):
+        own = [owns_triple(i, j, k, n_v, g) for i, j, k in iter_triples(n_v)]
+        out.append({"arity": 3, "n_v": n_v, "grid": grid_dict(g),
+                    "rank": [o[0] for o in own], "stage": [o[1] for o in own]})
+    return out
+
+
+def output_cases():
+    """Reference run + write_run_output: per-file sha256 and the manifest."""
+    import hashlib
+    import tempfile
+
+    from propsim.io import MetricOutputSpec, read_manifest, write_run_output
+
+    specs = [
+        ("uniform", 2, "double", 777, 48, DecompGrid(), 11, 0, None, "czekanowski"),
+        ("random-exact", 2, "double", 64, 24, DecompGrid(n_pv=3, n_pr=2), 401, 11, None,
+         "czekanowski"),
+        ("uniform", 2, "single", 1000, 120, DecompGrid(n_pf=4, n_pv=2), 17, 0, None,
+         "czekanowski"),
+        ("random-exact", 3, "double", 64, 24, DecompGrid(n_pv=2, n_pr=3), 402, 11, None,
+         "czekanowski"),
+        ("random-exact", 3, "double", 64, 24, DecompGrid(n_pv=2, n_st=2), 402, 11, 1,
+         "czekanowski"),
+        ("uniform", 3, "single", 300, 24, DecompGrid(n_pf=4, n_pv=2), 29, 0, None,
+         "czekanowski"),
+        ("random-exact", 2, "single", 777, 96, DecompGrid(n_pv=3, n_pr=2), 31, 1, None,
+         "sorenson"),
+    ]
+    out = []
+    for kind, arity, prec, n_f, n_v, g, seed, bits, stage, metric in specs:
+        if kind == "uniform":
+            src = ArraySource(uniform(seed, n_f, n_v, prec))
+        else:
+            src = gen_random_exact(seed, n_f, n_v, bits)
+        prob = Problem(arity, n_f, n_v, src, prec, metric=metric)
+        res = run_2way(prob, g) if arity == 2 else run_3way(prob, g, stage=stage)
+        for mode in ("full", "byte"):
+            with tempfile.TemporaryDirectory() as d:
+                write_run_output(res, MetricOutputSpec(d, mode), source={"kind": kind})
+                files = {}
+                for r in range(g.n_p):
+                    blob = Path(d, f"metrics_{r}.bin").read_bytes()
+                    files[str(r)] = [len(blob), hashlib.sha256(blob).hexdigest()]
+                out.append({"kind": kind, "arity": arity, "precision": prec, "n_f": n_f,
+                            "n_v": n_v, "grid": grid_dict(g), "seed": seed, "bits": bits,
+                            "stage": stage, "metric": metric, "mode": mode, "files": files,
+                            "manifest": read_manifest(Path(d, "manifest.txt"))})
+    return out
 
 
 if __name__ == "__main__":
