@@ -75,10 +75,52 @@ def main():
             print(json.dumps({"arity": c["arity"], "precision": c["precision"], "n_f": c["n_f"],
                               "n_v": c["n_v"], "grid": c["grid"], "checksum": res.checksum.hex,
                               "want": want, "ok": ok, "elapsed": res.elapsed}), flush=True)
+    bad += check_outputs(gold, world, rank)
     t = torch.tensor([bad], device="cuda")
     dist.broadcast(t, 0)
     dist.destroy_process_group()
     sys.exit(1 if int(t.item()) else 0)
+
+
+def check_outputs(gold, world, rank) -> int:
+    """NCCL runs written as metrics directories (collective write_run_output:
+    every process writes its own metrics_<rank>.bin) against the directories
+    the reference wrote (golden sha256)."""
+    import hashlib
+    import tempfile
+
+    from paper_1705_08210_b200 import output as OUT
+
+    bad = 0
+    for c in gold["outputs"]:
+        g = c["grid"]
+        if g["n_pf"] * g["n_pv"] * g["n_pr"] != world:
+            continue
+        if c["kind"] == "uniform":
+            src = P.gen_uniform(c["seed"], c["n_f"], c["n_v"])
+        else:
+            src = P.gen_random_exact(c["seed"], c["n_f"], c["n_v"], c["bits"])
+        prob = P.Problem(c["arity"], c["n_f"], c["n_v"], src, c["precision"], c["metric"])
+        grid = P.DecompGrid(**g)
+        if c["arity"] == 2:
+            res = P.run_2way(prob, grid, transport="nccl")
+        else:
+            res = P.run_3way(prob, grid, stage=c["stage"], transport="nccl")
+        d = [tempfile.mkdtemp(prefix="psim_out_") if rank == 0 else None]
+        dist.broadcast_object_list(d, 0)
+        OUT.write_run_output(res, OUT.MetricOutputSpec(d[0], c["mode"]),
+                             source={"kind": c["kind"]})
+        if rank == 0:
+            ok = all(hashlib.sha256(Path(d[0], f"metrics_{r}.bin").read_bytes()).hexdigest() == h
+                     for r, (_, h) in c["files"].items())
+            m = OUT.read_manifest(Path(d[0], "manifest.txt"))
+            ok &= all(m[k] == v for k, v in c["manifest"].items()
+                      if k not in ("transport", "kernel"))
+            bad += not ok
+            print(json.dumps({"output": True, "arity": c["arity"], "mode": c["mode"],
+                              "grid": g, "stage": c["stage"], "ok": ok}), flush=True)
+        dist.barrier()
+    return bad
 
 
 if __name__ == "__main__":
