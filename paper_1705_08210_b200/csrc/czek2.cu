@@ -66,13 +66,19 @@ __global__ void __launch_bounds__(kNT, C::MINB) k_minplus2(const Args2<typename 
     asm volatile("griddepcontrol.wait;" ::: "memory");
     return;  // left of the diagonal inside a diagonal band (uniform per CTA)
   }
+  T acc[C::TM][C::TN];
+  {
+    const int64_t row0 = (int64_t)bi * C::BM, col0 = (int64_t)bj * C::BN;
+    minplus_tile<C, false>(a.W + row0 * a.ldw, a.ldw, (int)min64(C::BM, a.m_end - row0),
+                           a.V + col0 * a.ldv, a.ldv, (int)min64(C::BN, a.n - col0), nullptr,
+                           a.n_f, acc, smem);
+  }
+  // the tile is decoded again rather than kept live across the mainloop
+  band_tile((int64_t)blockIdx.x, a.row_pref, a.nbands, a.band, a.row_tile0,
+            a.row_tile0 + a.tiles_m, C::BM, C::BN, a.diagonal, bi, bj);
   const int64_t row0 = (int64_t)bi * C::BM, col0 = (int64_t)bj * C::BN;
   const int rows = (int)min64(C::BM, a.m_end - row0);
   const int cols = (int)min64(C::BN, a.n - col0);
-
-  T acc[C::TM][C::TN];
-  minplus_tile<C, false>(a.W + row0 * a.ldw, a.ldw, rows, a.V + col0 * a.ldv, a.ldv, cols,
-                         nullptr, a.n_f, acc, smem);
 
   const int ty = thread_ty(), tx = thread_tx();
   if (MODE == kCzek2) {

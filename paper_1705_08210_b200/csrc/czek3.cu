@@ -44,6 +44,44 @@ __device__ __forceinline__ T czek3_value(const Czek3Box& b, int64_t ai, int64_t 
   return zero ? T(0) : Traits<T>::div(Traits<T>::mul(T(1.5), n3), d);
 }
 
+// One CTA's tile of a box: pivot j (index lo in the box's J range), the
+// tile's rows / cols, and their local columns in blocks A / C.
+struct Tile3 {
+  int64_t lo, j, ncols, r0, c0, ia, kc, jb;
+  int rows, cols;
+};
+
+// tile_pref is read with volatile loads (ld_pref) so the second decode after
+// the mainloop is recomputed, not kept live in registers across it.
+template <class C>
+__device__ __forceinline__ Tile3 decode3(const Czek3Box& b, const int64_t* tile_pref, int64_t nJ) {
+  Tile3 d;
+  // locate pivot j: largest lo with tile_pref[lo] <= blockIdx.x
+  const int64_t t = blockIdx.x;
+  int64_t lo = 0, hi = nJ;  // invariant tile_pref[lo] <= t < tile_pref[hi]
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (ld_pref(tile_pref + mid) <= t) lo = mid; else hi = mid;
+  }
+  d.lo = lo;
+  d.j = b.j0 + lo;
+  const int64_t ihi = min64(b.i1, d.j);
+  const int64_t klo = max64(b.k0, d.j + 1);
+  const int64_t nrows = ihi - b.i0;
+  d.ncols = b.k1 - klo;
+  const int64_t tiles_k = (d.ncols + C::BN - 1) / C::BN;
+  const int64_t lt = t - ld_pref(tile_pref + lo);
+  const int64_t ti = lt / tiles_k, tk = lt - ti * tiles_k;
+  d.r0 = ti * C::BM;
+  d.c0 = tk * C::BN;
+  d.rows = (int)min64(C::BM, nrows - d.r0);
+  d.cols = (int)min64(C::BN, d.ncols - d.c0);
+  d.ia = b.i0 - b.a0 + d.r0;   // local column of the tile's first i in block A
+  d.kc = klo - b.c0 + d.c0;    // local column of the tile's first k in block C
+  d.jb = d.j - b.b0;           // local column of j in block B
+  return d;
+}
+
 // RAW = true writes the n_ijk partial sums (field-split path) instead of values.
 template <class C, bool RAW>
 __global__ void __launch_bounds__(kNT, C::MINB)
@@ -53,34 +91,19 @@ __global__ void __launch_bounds__(kNT, C::MINB)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* smem = reinterpret_cast<T*>(smem_raw);
 
-  // locate pivot j: largest jj with tile_pref[jj] <= blockIdx.x
-  const int64_t t = blockIdx.x;
-  int64_t lo = 0, hi = nJ;  // invariant tile_pref[lo] <= t < tile_pref[hi]
-  while (hi - lo > 1) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (tile_pref[mid] <= t) lo = mid; else hi = mid;
-  }
-  const int64_t j = b.j0 + lo;
-  const int64_t ihi = min64(b.i1, j);
-  const int64_t klo = max64(b.k0, j + 1);
-  const int64_t nrows = ihi - b.i0, ncols = b.k1 - klo;
-  const int64_t tiles_k = (ncols + C::BN - 1) / C::BN;
-  const int64_t lt = t - tile_pref[lo];
-  const int64_t ti = lt / tiles_k, tk = lt - ti * tiles_k;
-  const int64_t r0 = ti * C::BM, c0 = tk * C::BN;
-  const int rows = (int)min64(C::BM, nrows - r0);
-  const int cols = (int)min64(C::BN, ncols - c0);
-
-  const T* VA = static_cast<const T*>(b.VA);
-  const T* VB = static_cast<const T*>(b.VB);
-  const T* VC = static_cast<const T*>(b.VC);
-  const int64_t ia = b.i0 - b.a0 + r0;   // local column of the tile's first i in block A
-  const int64_t kc = klo - b.c0 + c0;    // local column of the tile's first k in block C
-  const int64_t jb = j - b.b0;           // local column of j in block B
-
   T acc[C::TM][C::TN];
-  minplus_tile<C, true>(VA + ia * b.ldA, b.ldA, rows, VC + kc * b.ldC, b.ldC, cols,
-                        VB + jb * b.ldB, b.n_f, acc, smem);
+  {
+    const Tile3 d = decode3<C>(b, tile_pref, nJ);
+    minplus_tile<C, true>(static_cast<const T*>(b.VA) + d.ia * b.ldA, b.ldA, d.rows,
+                          static_cast<const T*>(b.VC) + d.kc * b.ldC, b.ldC, d.cols,
+                          static_cast<const T*>(b.VB) + d.jb * b.ldB, b.n_f, acc, smem);
+  }
+  // decoded again (measured: keeping the tile state live across the mainloop
+  // costs registers and ~4% of the mainloop's issue rate)
+  const Tile3 d = decode3<C>(b, tile_pref, nJ);
+  const int64_t lo = d.lo, j = d.j, ncols = d.ncols, r0 = d.r0, c0 = d.c0;
+  const int64_t ia = d.ia, kc = d.kc, jb = d.jb;
+  const int rows = d.rows, cols = d.cols;
 
   T* out = static_cast<T*>(b.vals);
   const int64_t obase = out_pref[lo];

@@ -337,11 +337,11 @@ __device__ __forceinline__ bool band_tile(int64_t t, const int64_t* __restrict__
   int64_t lo = 0, hi = nbands;
   while (hi - lo > 1) {
     const int64_t mid = (lo + hi) >> 1;
-    if (band_pref[mid] <= t) lo = mid; else hi = mid;
+    if (ld_pref(band_pref + mid) <= t) lo = mid; else hi = mid;
   }
   const int64_t r0 = row_tile0 + lo * G;
   const int64_t rows = min64(G, row_tile_end - r0);
-  const int64_t u = t - band_pref[lo];
+  const int64_t u = t - ld_pref(band_pref + lo);
   const int64_t b = r0 + u % rows;
   const int64_t c = first_col_tile(r0, bm, bn, diagonal) + u / rows;
   bi = (int)b;

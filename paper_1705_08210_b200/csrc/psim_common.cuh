@@ -162,4 +162,12 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// Volatile read-only load: never CSE'd or hoisted, so tile decodes repeated
+// after a mainloop are recomputed instead of held live in registers.
+__device__ __forceinline__ int64_t ld_pref(const int64_t* p) {
+  int64_t v;
+  asm volatile("ld.global.nc.s64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+
 }  // namespace psim
