@@ -387,6 +387,9 @@ def e2e_2way(P, prob, grid, precision, args, total_cmp, world, rank) -> dict:
             "h2d_bytes_per_step": prob.n_f * prob.n_v * isz,
             "d2h_bytes_per_step": math.comb(prob.n_v, 2) * isz + 32 * world,
             "seconds_per_step": el, "checksum": cks,
+            "values_path": ("zero-copy: the fused kernel stores every value into pinned host "
+                            "memory" if os.environ.get("PSIM_HOST_OUTPUT", "direct") != "bands"
+                            else "row bands in HBM, D2H copies overlapped with the next band"),
             "api": f"paper_1705_08210_b200.run_2way(Problem(2, n_f, n_v, pinned slab source), "
                    f"grid, transport='{transport}', host_values=True)"}
 

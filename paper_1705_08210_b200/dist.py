@@ -340,12 +340,16 @@ class Runner2:
         total, r0, r1 = reduce_scatter_rows(part, m, n, t.diagonal, self.coords.p_f, g.n_pf,
                                             self.group,
                                             lambda dst, src: D.fold_(dst, src, self.code))
+        direct = self.sink is not None and self.sink.direct
         keep = self.keep or self.sink is not None
-        vals = torch.empty(total.numel(), dtype=tdt, device=self.dev) if keep else None
+        if direct:  # zero-copy: the epilogue writes pinned host memory
+            vals = self.sink.buffer(total.numel(), tdt)
+        else:
+            vals = torch.empty(total.numel(), dtype=tdt, device=self.dev) if keep else None
         if r1 > r0:
             finish_numerators(self.code, total, r0, r1, m, n, t.diagonal, s_row[t.r0:],
                               s_col[t.c0:], W.v0 + t.r0, V.v0 + t.c0, p.n_v, vals, self.acc)
-        if self.sink is not None:
+        if self.sink is not None and not direct:
             host = self.sink.buffer(vals.numel(), tdt)
             self.sink.copy(host, vals, 0, vals.numel())
             vals = host

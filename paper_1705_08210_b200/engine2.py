@@ -50,13 +50,23 @@ def fold_sums(parts: list[torch.Tensor], code: int) -> torch.Tensor:
 
 
 class HostSink:
-    """Streams finished row bands of device values into pinned host memory on a
-    side stream, overlapping the D2H copy with the next band's kernel.
-    Pinned buffers come from torch's caching host allocator (reused once the
-    previous result is released)."""
+    """Delivers a run's values into pinned host memory.
 
-    def __init__(self, bands: int = 8):
+    ``direct`` (default): the fused kernels store each value straight into
+    the pinned buffer (zero-copy: a device store to a UVA host address goes
+    over PCIe as the epilogue runs), so a task is ONE launch and nothing is
+    left to copy when it ends. ``bands`` (PSIM_HOST_OUTPUT=bands): values go
+    to HBM and finished row bands are copied D2H on a side stream while the
+    next band's kernel runs. Pinned buffers come from torch's caching host
+    allocator (reused once the previous result is released)."""
+
+    def __init__(self, bands: int = 8, direct: bool | None = None):
+        import os
+
         self.bands = bands
+        if direct is None:
+            direct = os.environ.get("PSIM_HOST_OUTPUT", "direct") != "bands"
+        self.direct = direct
         self.stream = torch.cuda.Stream()
 
     def buffer(self, count: int, dtype) -> torch.Tensor:
@@ -82,8 +92,13 @@ def run_task(code: int, problem, grid, task: Task2, row_blocks: list, col_blocks
     count = D.pair_count(m, n, task.diagonal)
     dev = acc.device
     tdt = D.torch_dtype(problem.precision)
-    vals = torch.empty(count, dtype=tdt, device=dev) if keep_values or sink else None
     W0, V0 = row_blocks[0], col_blocks[0]
+    if len(row_blocks) == 1 and sink is not None and sink.direct:
+        host = sink.buffer(count, tdt)  # the kernel stores the values into it
+        D.czek2_block(code, W0, task.r0, task.r1, V0, task.c0, task.c1, s_row, s_col,
+                      task.diagonal, problem.n_v, host, acc)
+        return PairPiece(W0.v0 + task.r0, V0.v0 + task.c0, m, n, task.diagonal, 0, m, host)
+    vals = torch.empty(count, dtype=tdt, device=dev) if keep_values or sink else None
     if len(row_blocks) == 1 and sink is not None:
         host = sink.buffer(count, tdt)
         bm, _ = N.tile_shape(code)
@@ -97,6 +112,8 @@ def run_task(code: int, problem, grid, task: Task2, row_blocks: list, col_blocks
         D.czek2_block(code, W0, task.r0, task.r1, V0, task.c0, task.c1, s_row, s_col,
                       task.diagonal, problem.n_v, vals, acc)
     else:
+        if sink is not None and sink.direct:  # zero-copy: the epilogue writes pinned host memory
+            vals = sink.buffer(count, tdt)
         total = torch.empty(count, dtype=tdt, device=dev)
         D.mgemm_packed(code, W0, task.r0, task.r1, V0, task.c0, task.c1, task.diagonal, total)
         part = torch.empty_like(total)
@@ -106,7 +123,7 @@ def run_task(code: int, problem, grid, task: Task2, row_blocks: list, col_blocks
         finish_numerators(code, total, 0, m, m, n, task.diagonal,
                           s_row[task.r0:], s_col[task.c0:], W0.v0 + task.r0, V0.v0 + task.c0,
                           problem.n_v, vals, acc)
-        if sink is not None:
+        if sink is not None and not sink.direct:
             host = sink.buffer(count, tdt)
             sink.copy(host, vals, 0, count)
             vals = host
@@ -139,7 +156,7 @@ def run_local(problem, grid, balance: str = "split", keep_values: bool = True,
     acc = D.new_acc(dev)
     pieces = []
     count = 0
-    specs = []  # single-slab tasks without host streaming: batched into shared grids
+    specs = []  # single-slab tasks (device or zero-copy host values): batched into shared grids
     tdt = D.torch_dtype(problem.precision)
     bits = {p_v: D.pack_bits(blocks[0, p_v]) for p_v in range(grid.n_pv)} if bitpacked else None
     for p_r in range(grid.n_pr):
@@ -151,21 +168,28 @@ def run_local(problem, grid, balance: str = "split", keep_values: bool = True,
                 cols = [blocks[p_f, ev.col_block] for p_f in range(grid.n_pf)]
                 m, n = ev.r1 - ev.r0, ev.c1 - ev.c0
                 if bitpacked:  # Sorenson on 0/1 data: AND + POPC mainloop
-                    vals = torch.empty(D.pair_count(m, n, ev.diagonal), dtype=tdt, device=dev)
+                    cnt = D.pair_count(m, n, ev.diagonal)
+                    if sink is not None and sink.direct:
+                        vals = sink.buffer(cnt, tdt)  # zero-copy host output
+                    else:
+                        vals = torch.empty(cnt, dtype=tdt, device=dev)
                     Wb, Vb = bits[ev.row_block], bits[ev.col_block]
                     D.sorenson2_block(code, Wb, ev.r0, ev.r1, Vb, ev.c0, ev.c1,
                                       sums[ev.row_block], sums[ev.col_block], ev.diagonal,
                                       problem.n_v, vals, acc)
-                    if sink is not None:
+                    if sink is not None and not sink.direct:
                         host = sink.buffer(vals.numel(), tdt)
                         sink.copy(host, vals, 0, vals.numel())
                         vals = host
                     elif not keep_values:
                         vals = None
                     piece = PairPiece(Wb.v0 + ev.r0, Vb.v0 + ev.c0, m, n, ev.diagonal, 0, m, vals)
-                elif grid.n_pf == 1 and sink is None:
-                    vals = torch.empty(D.pair_count(m, n, ev.diagonal), dtype=tdt,
-                                       device=dev) if keep_values else None
+                elif grid.n_pf == 1 and (sink is None or sink.direct):
+                    cnt = D.pair_count(m, n, ev.diagonal)
+                    if sink is not None:  # zero-copy: the kernel writes pinned host memory
+                        vals = sink.buffer(cnt, tdt)
+                    else:
+                        vals = torch.empty(cnt, dtype=tdt, device=dev) if keep_values else None
                     W, V = rows[0], cols[0]
                     specs.append((W, ev.r0, ev.r1, V, ev.c0, ev.c1, sums[ev.row_block],
                                   sums[ev.col_block], ev.diagonal, vals))

@@ -159,18 +159,22 @@ def run_boxes(code, problem, boxes, blocks, sums, tables, acc, keep_values, piec
     count = 0
     tdt = D.torch_dtype(problem.precision)
     dev = acc.device
-    if sink is not None:  # pivot-range sub-boxes so each D2H overlaps the next launch
+    banded = sink is not None and not sink.direct
+    if banded:  # pivot-range sub-boxes so each D2H overlaps the next launch
         boxes = [sub for b in boxes for sub in pivot_chunks(b, sink.bands)]
     for box in boxes:
         probe = box_struct(box, blocks, sums, tables, problem.n_f, problem.n_v, None, acc)
         n_out, _ = box_plan(probe)
         if n_out == 0:
             continue
-        keep = keep_values or sink is not None
-        vals = torch.empty(n_out, dtype=tdt, device=dev) if keep else None
+        if sink is not None and sink.direct:  # zero-copy: the kernel writes pinned host memory
+            vals = sink.buffer(n_out, tdt)
+        else:
+            keep = keep_values or sink is not None
+            vals = torch.empty(n_out, dtype=tdt, device=dev) if keep else None
         b = box_struct(box, blocks, sums, tables, problem.n_f, problem.n_v, vals, acc)
         N.call("psim_czek3_box", code, C.byref(b), D.stream_ptr())
-        if sink is not None:
+        if banded:
             host = sink.buffer(n_out, tdt)
             sink.copy(host, vals, 0, n_out)
             vals = host

@@ -307,21 +307,29 @@ def test_large_field_split_sampled():
     assert res.checksum.hex == O.checksum_hex(np.arange(len(vals)), vals)
 
 
-def test_band_launches_equal_single_launch():
-    """host_values=True runs the diagonal task as row bands with overlapped
-    D2H copies; values and checksum must equal the single-launch run."""
+@pytest.mark.parametrize("mode", ["direct", "bands"])
+def test_band_launches_equal_single_launch(mode, monkeypatch):
+    """host_values=True: zero-copy ("direct": the kernel stores into pinned
+    host memory) or row bands with overlapped D2H copies ("bands"); values
+    and checksum must equal the device-resident run, for a single slab, a
+    circulant grid and a field split."""
+    monkeypatch.setenv("PSIM_HOST_OUTPUT", mode)
     P = _api()
     spec = P.gen_uniform(4, 3000, 3000)
     prob = P.Problem(2, 3000, 3000, spec, "double")
-    a = P.run_2way(prob, P.DecompGrid())
-    b = P.run_2way(prob, P.DecompGrid(), host_values=True)
-    assert a.checksum == b.checksum
-    assert (a.records.values.view(np.uint64) == b.records.values.view(np.uint64)).all()
+    for grid in (P.DecompGrid(), P.DecompGrid(n_pv=3, n_pr=2), P.DecompGrid(n_pf=2, n_pv=2)):
+        a = P.run_2way(prob, grid)
+        b = P.run_2way(prob, grid, host_values=True)
+        assert a.checksum == b.checksum
+        assert (a.records.values.view(np.uint64) == b.records.values.view(np.uint64)).all()
 
 
-def test_3way_streamed_host_values_equal_device_run():
-    """run_3way(host_values=True) splits boxes into pivot ranges and streams
-    them to pinned host memory; results must equal the plain run."""
+@pytest.mark.parametrize("mode", ["direct", "bands"])
+def test_3way_streamed_host_values_equal_device_run(mode, monkeypatch):
+    """run_3way(host_values=True) writes each box's values to pinned host
+    memory (zero-copy, or pivot-range chunks copied while the next computes);
+    results must equal the plain run."""
+    monkeypatch.setenv("PSIM_HOST_OUTPUT", mode)
     P = _api()
     prob = P.Problem(3, 500, 96, P.gen_uniform(12, 500, 96), "single")
     for grid in (P.DecompGrid(), P.DecompGrid(n_pv=2, n_st=2)):
