@@ -153,6 +153,25 @@ int psim_pack_bits(int dtype, const void* V, int64_t n_fp, int64_t n_vp, int64_t
  * layout and checksum of psim_czek2_block; s_row / s_col are the dense
  * column sums. No row bands. */
 int psim_sorenson2_block(int dtype, const psim_block2_t* task, void* stream);
+/* One whole diagonal task (the single-slab run, metrics2.py:149-158) over a
+ * block still in PINNED host memory (vector i at host + i*host_ld elements):
+ * the block is copied into task->W (== task->V, device, padded ld) by the
+ * copy engine on copy_stream in chunks of `chunk` vectors from the last one
+ * down, each followed by ready[c] = 1; the fused kernel on compute_stream
+ * starts at the bottom tiles as soon as their chunk lands. The column sums
+ * are folded in the mainloop of each row tile's first (diagonal) CTA, which
+ * WRITES them to task->s_row (n entries, device) and publishes them with a
+ * flag; task->s_col is not used. vals may be device or pinned host memory.
+ * ready: device scratch of ceil(n / chunk) + ceil(n / BM) words (BM from
+ * psim_tile_shape). The caller validates the block afterwards
+ * (psim_check_block) and must keep `host` alive until copy_stream completes. */
+int psim_czek2_streamed(int dtype, const psim_block2_t* task, const void* host, int64_t host_ld,
+                        int64_t chunk, unsigned* ready, void* compute_stream,
+                        void* copy_stream);
+/* Wait statistics of streamed runs since the last reset (host, synchronous):
+ * out4 = {ns tiles waited for input chunks, ns waited for column sums,
+ * number of column-sum waits, longest single wait in ns}. */
+int psim_stream_stats(unsigned long long* out4, int reset);
 /* 2-way epilogue from reduced packed numerators, rows [r0, r1) of a task's
  * packed layout (field-axis path, metrics2.py:156-158). N and vals point at
  * the first entry of row r0. */

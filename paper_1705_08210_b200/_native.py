@@ -83,6 +83,9 @@ SIGNATURES = {
         [C.c_int, c_vp, c_i64, c_i64, c_i64, c_i64, C.c_int, c_vp, c_vp, c_i64, c_i64, c_i64,
          c_vp, c_vp, c_vp]),
     "psim_fold_add": (C.c_int, [C.c_int, c_vp, c_vp, c_i64, c_vp]),
+    "psim_czek2_streamed": (C.c_int, [C.c_int, C.POINTER(Block2), c_vp, c_i64, c_i64, c_vp,
+                                      c_vp, c_vp]),
+    "psim_stream_stats": (C.c_int, [C.POINTER(C.c_uint64), C.c_int]),
     "psim_quantize_bytes": (C.c_int, [C.c_int, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "psim_box3_plan": (C.c_int, [C.c_int, C.POINTER(Box3), C.POINTER(c_i64), C.POINTER(c_i64)]),
     "psim_czek3_box": (C.c_int, [C.c_int, C.POINTER(Box3), c_vp]),

@@ -220,6 +220,40 @@ static int check_task2(int dtype, const psim_block2_t* t) {
   return PSIM_OK;
 }
 
+int psim_czek2_streamed(int dtype, const psim_block2_t* t, const void* host, int64_t host_ld,
+                        int64_t chunk, unsigned* ready, void* compute_stream,
+                        void* copy_stream) {
+  if (int r = check_dtype(dtype)) return r;
+  if (!t) return fail(PSIM_ECONFIG, "task is NULL");
+  if (t->n_f < 1 || t->m < 1 || t->m != t->n || !t->diagonal || t->W != t->V ||
+      t->ldw != t->ldv || t->g_row != t->g_col || t->row_begin || t->row_end)
+    return fail(PSIM_ECONFIG, "streamed run needs one whole diagonal task (W == V, m == n)");
+  if (int r = check_operand(dtype, t->W, t->ldw, t->n_f, "W")) return r;
+  if (!t->acc || !t->s_row) return fail(PSIM_ECONFIG, "acc / s_row (sums out) is NULL");
+  if (t->g_row < 0 || t->g_row + t->m > t->n_v) return fail(PSIM_ECONFIG, "task outside [0, n_v)");
+  if (!host || host_ld < t->n_f || !ready || chunk < 1)
+    return fail(PSIM_ECONFIG, "bad host block / ready flags / chunk");
+  int bm = 0, bn = 0;
+  psim::tile_shape(dtype, &bm, &bn);
+  if ((t->n + chunk - 1) / chunk + (t->n + bm - 1) / bm > psim::kStreamMaxFlags)
+    return fail(PSIM_ECONFIG, "too many chunks / row tiles (flags > %lld)",
+                (long long)psim::kStreamMaxFlags);
+  if (compute_stream == copy_stream) return fail(PSIM_ECONFIG, "copy stream must differ");
+  cudaPointerAttributes pa{};
+  if (cudaPointerGetAttributes(&pa, host) != cudaSuccess || pa.type != cudaMemoryTypeHost) {
+    cudaGetLastError();
+    return fail(PSIM_ECONFIG, "host block must be pinned (page-locked) memory");
+  }
+  return cuda_status(psim::czek2_streamed(dtype, *t, host, host_ld, chunk, ready,
+                                          S(compute_stream), S(copy_stream)),
+                     "psim_czek2_streamed");
+}
+
+int psim_stream_stats(unsigned long long* out4, int reset) {
+  if (!out4) return fail(PSIM_ECONFIG, "NULL argument");
+  return cuda_status(psim::stream_stats(out4, reset), "psim_stream_stats");
+}
+
 int psim_czek2_from_numerators(int dtype, const void* N, int64_t r0, int64_t r1, int64_t m,
                                int64_t n, int diagonal, const void* s_row, const void* s_col,
                                int64_t g_row, int64_t g_col, int64_t n_v, void* vals,

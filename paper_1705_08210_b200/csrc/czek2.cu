@@ -21,6 +21,8 @@ enum Mode2 : int {
   kCzek2 = 0,      // values + checksum (+ degenerate count)
   kRawCol = 1,     // numerators, column-major M[i + j*ldm]; diagonal mirrors to a full square
   kRawPacked = 2,  // numerators in the packed value layout (triangle or row-major rectangle)
+  kCzek2Streamed = 3,  // kCzek2 while the block is still arriving: tiles bottom-up, each
+                       // waits for its input chunk's ready flag; sums computed in the tile
 };
 
 template <typename T>
@@ -43,7 +45,107 @@ struct Args2 {
   int64_t m_end;              // rows >= m_end are outside the band
   int64_t band, nbands;       // rasterisation: row-tiles per band, bands in the launch
   const int64_t* row_pref;    // tiles before each band (device), see band_tile
+  const unsigned* ready;      // kCzek2Streamed: ready[c] != 0 once vectors of chunk c landed
+  int64_t chunk;              // kCzek2Streamed: vectors per chunk
+  T* sums;                    // kCzek2Streamed: column sums, published per row tile
+  unsigned* sum_ready;        // kCzek2Streamed: sum_ready[r] != 0 once row tile r's are in
 };
+
+// kCzek2Streamed: the host uploads the block in chunks from the LAST vector
+// down (copy engine, flag after each chunk), so a tile whose lowest vector is
+// v may start once chunk(v)'s flag is set. Bounded spin: a flag that never
+// arrives traps (a kernel error) instead of hanging the GPU.
+// Wait statistics of streamed runs (psim_stream_stats): total ns spent
+// waiting for input chunks / for column sums, count of sum waits, max wait.
+__device__ unsigned long long g_stream_wait[4];
+
+__device__ __forceinline__ void wait_ready(const unsigned* flag, int kind) {
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (uint64_t t = t0;;) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (v) {
+      if (t > t0) {
+        atomicAdd(&g_stream_wait[kind], (unsigned long long)(t - t0));
+        if (kind == 1) atomicAdd(&g_stream_wait[2], 1ull);
+        atomicMax(&g_stream_wait[3], (unsigned long long)(t - t0));
+      }
+      return;
+    }
+    __nanosleep(512);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 20000000000ull) __trap();  // 20 s
+  }
+}
+
+cudaError_t stream_stats(unsigned long long* out4, int reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out4, g_stream_wait, sizeof(g_stream_wait));
+  if (e == cudaSuccess && reset) {
+    const unsigned long long z[4] = {0, 0, 0, 0};
+    e = cudaMemcpyToSymbol(g_stream_wait, z, sizeof(z));
+  }
+  return e;
+}
+
+// kCzek2Streamed CTA order: bands bottom-up; each band starts with one
+// column-sum CTA per row tile of the band, then the band's tiles in
+// band_tile order. Band b holds launch tiles [pref[b], pref[b+1]) and row
+// tiles [b*G, min((b+1)*G, tiles_m)), so with its sum CTAs it spans
+// [P(b), P(b+1)) of the extended order, P(b) = pref[b] + b*G (P(nbands) =
+// total + tiles_m); bottom-up it sits at [P_end - P(b+1), P_end - P(b)).
+// Returns the band_tile index, or -1 - r for the sum CTA of row tile r.
+template <typename T>
+__device__ __forceinline__ int64_t streamed_tile(const Args2<T>& a) {
+  auto P = [&](int64_t b) {
+    return ld_pref(a.row_pref + b) + (b == a.nbands ? a.tiles_m : b * a.band);
+  };
+  const int64_t end = P(a.nbands);
+  const int64_t t = blockIdx.x, x = end - 1 - t;
+  int64_t lo = 0, hi = a.nbands;
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (P(mid) <= x) lo = mid; else hi = mid;
+  }
+  const int64_t off = t - (end - P(lo + 1));
+  const int64_t rows = min64(a.band, a.tiles_m - lo * a.band);
+  if (off < rows) return -1 - (lo * a.band + off);
+  return ld_pref(a.row_pref + lo) + (off - rows);
+}
+
+// Column sums of the 128 (BM) vectors of row tile r, each a sequential
+// ascending-q fold from +0 (k_colsum's order), staged 32 fields at a time
+// through shared memory with coalesced loads; published with sum_ready[r].
+template <class C>
+__device__ void streamed_row_sums(const Args2<typename C::T>& a, int64_t r,
+                                  typename C::T* smem) {
+  using T = typename C::T;
+  const int64_t v0 = r * C::BM;
+  const int nv = (int)min64(C::BM, a.n - v0);
+  if (threadIdx.x == 0) wait_ready(a.ready + v0 / a.chunk, 0);
+  __syncthreads();
+  T (*tile)[33] = reinterpret_cast<T (*)[33]>(smem);  // [BM][33]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T acc = T(0);
+  for (int64_t q0 = 0; q0 < a.n_f; q0 += 32) {
+    const int64_t q = q0 + lane;
+    for (int lv = warp; lv < C::BM; lv += kNT / 32)
+      tile[lv][lane] = (lv < nv && q < a.n_f) ? __ldcg(a.W + (v0 + lv) * a.ldw + q) : T(0);
+    __syncthreads();
+    if (threadIdx.x < C::BM) {
+      const int cnt = (int)min64(32, a.n_f - q0);
+      for (int k = 0; k < cnt; ++k) acc = Traits<T>::add(acc, tile[threadIdx.x][k]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < nv) a.sums[v0 + threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.sum_ready + r), "r"(1u)
+                 : "memory");
+  }
+}
 
 // Position of local pair (i, j) in the packed layout shared by values and
 // packed numerators: the block triangle in canonical order (diagonal task)
@@ -60,42 +162,66 @@ __global__ void __launch_bounds__(kNT, C::MINB) k_minplus2(const Args2<typename 
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* smem = reinterpret_cast<T*>(smem_raw);
+  constexpr bool STREAMED = MODE == kCzek2Streamed;
+  // streamed: bands bottom-up (their input arrives first), each led by the
+  // CTAs that publish its row tiles' column sums
+  int64_t tb = blockIdx.x;
+  if constexpr (STREAMED) {
+    tb = streamed_tile(a);
+    if (tb < 0) {
+      streamed_row_sums<C>(a, -1 - tb, smem);
+      return;
+    }
+  }
   int bi, bj;
-  if (!band_tile((int64_t)blockIdx.x, a.row_pref, a.nbands, a.band, a.row_tile0,
-                 a.row_tile0 + a.tiles_m, C::BM, C::BN, a.diagonal, bi, bj)) {
+  if (!band_tile(tb, a.row_pref, a.nbands, a.band, a.row_tile0, a.row_tile0 + a.tiles_m, C::BM,
+                 C::BN, a.diagonal, bi, bj)) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     return;  // left of the diagonal inside a diagonal band (uniform per CTA)
   }
   T acc[C::TM][C::TN];
   {
     const int64_t row0 = (int64_t)bi * C::BM, col0 = (int64_t)bj * C::BN;
+    if (STREAMED) {
+      if (threadIdx.x == 0) wait_ready(a.ready + min64(row0, col0) / a.chunk, 0);
+      __syncthreads();
+    }
     minplus_tile<C, false>(a.W + row0 * a.ldw, a.ldw, (int)min64(C::BM, a.m_end - row0),
                            a.V + col0 * a.ldv, a.ldv, (int)min64(C::BN, a.n - col0), nullptr,
                            a.n_f, acc, smem);
   }
   // the tile is decoded again rather than kept live across the mainloop
-  band_tile((int64_t)blockIdx.x, a.row_pref, a.nbands, a.band, a.row_tile0,
-            a.row_tile0 + a.tiles_m, C::BM, C::BN, a.diagonal, bi, bj);
+  band_tile(tb, a.row_pref, a.nbands, a.band, a.row_tile0, a.row_tile0 + a.tiles_m, C::BM, C::BN,
+            a.diagonal, bi, bj);
   const int64_t row0 = (int64_t)bi * C::BM, col0 = (int64_t)bj * C::BN;
   const int rows = (int)min64(C::BM, a.m_end - row0);
   const int cols = (int)min64(C::BN, a.n - col0);
-
+  if (STREAMED) {
+    // the sums of this tile's rows and columns: published by the owners of
+    // row tiles bi .. (col0 + cols - 1) / BM (columns lie at or right of the rows)
+    if (threadIdx.x == 0) {
+      wait_ready(a.sum_ready + bi, 1);
+      for (int64_t r = col0 / C::BM; r <= (col0 + cols - 1) / C::BM; ++r)
+        if (r != bi) wait_ready(a.sum_ready + r, 1);
+    }
+    __syncthreads();
+  }
   const int ty = thread_ty(), tx = thread_tx();
-  if (MODE == kCzek2) {
+  if (MODE == kCzek2 || STREAMED) {
     Cks c;
 #pragma unroll
     for (int mi = 0; mi < C::TM; ++mi) {
       const int li = ty + 16 * mi;
       if (li >= rows) continue;
       const int64_t i = row0 + li;
-      const T si = a.s_row[i];
+      const T si = STREAMED ? __ldcg(a.sums + i) : a.s_row[i];  // (L2: written this launch)
       const uint64_t gi = (uint64_t)(a.g_row + i);
 #pragma unroll
       for (int nj = 0; nj < C::TN; ++nj) {
         const int lj = tx + 16 * nj;
         const int64_t j = col0 + lj;
         if (lj >= cols || (a.diagonal && j <= i)) continue;
-        const T d = Traits<T>::add(si, a.s_col[j]);
+        const T d = Traits<T>::add(si, STREAMED ? __ldcg(a.sums + j) : a.s_col[j]);
         const bool zero = (d == T(0));
         const T v = zero ? T(0) : Traits<T>::div(Traits<T>::mul(T(2), acc[mi][nj]), d);
         if (a.out) a.out[packed_pos(a.diagonal, i, j, a.m, a.n)] = v;
@@ -205,13 +331,15 @@ static int64_t plan2(Args2<typename C::T>& a, int64_t row_begin, int64_t row_end
 template <class C, int MODE>
 static cudaError_t launch_group(Args2<typename C::T>* args, const int64_t* row_begin,
                                 const int64_t* row_end, int count, cudaStream_t st) {
+  constexpr int smem_bytes = C::SMEM_BYTES;
   cudaError_t e = cudaFuncSetAttribute(k_minplus2<C, MODE>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
   if (e != cudaSuccess) return e;
   int64_t total_bands = 0;
   int64_t* blocks = new int64_t[count];
   for (int k = 0; k < count; ++k) {
     blocks[k] = plan2<C>(args[k], row_begin ? row_begin[k] : 0, row_end ? row_end[k] : 0);
+    if (MODE == kCzek2Streamed && blocks[k] > 0) blocks[k] += args[k].tiles_m;  // sum CTAs
     if (blocks[k] > 0x7fffffffLL) e = cudaErrorInvalidConfiguration;
     if (blocks[k] > 0) total_bands += args[k].nbands + 1;
   }
@@ -233,7 +361,7 @@ static cudaError_t launch_group(Args2<typename C::T>* args, const int64_t* row_b
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)blocks[k]);
     cfg.blockDim = dim3(kNT);
-    cfg.dynamicSmemBytes = C::SMEM_BYTES;
+    cfg.dynamicSmemBytes = smem_bytes;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -289,6 +417,90 @@ cudaError_t czek2_tasks_t(const Czek2Block* tasks, int ntasks, cudaStream_t st) 
   delete[] rb;
   delete[] re;
   return e;
+}
+
+// Single diagonal task over a block that is still on the host: the block is
+// uploaded by the copy engine in chunks from the last vector down (2-D copies
+// into the padded layout, each followed by its ready flag), while the kernel
+// (tiles bottom-up) starts on the first chunk. See kCzek2Streamed.
+constexpr int64_t kMaxChunks = kStreamMaxFlags;
+
+static cudaError_t flag_sources(const unsigned** zeros, const unsigned** one) {
+  static unsigned* buf = nullptr;  // pinned [0] * kMaxChunks + [1]; never freed
+  static cudaError_t st = [] {
+    cudaError_t e = cudaHostAlloc(&buf, (kMaxChunks + 1) * sizeof(unsigned), cudaHostAllocDefault);
+    if (e == cudaSuccess) {
+      for (int64_t c = 0; c < kMaxChunks; ++c) buf[c] = 0;
+      buf[kMaxChunks] = 1;
+    }
+    return e;
+  }();
+  *zeros = buf;
+  *one = buf ? buf + kMaxChunks : nullptr;
+  return st;
+}
+
+template <typename T>
+cudaError_t czek2_streamed_t(const Czek2Block& t, const void* host, int64_t host_ld,
+                             int64_t chunk, unsigned* ready, cudaStream_t compute,
+                             cudaStream_t copy) {
+  using C = typename Prod<T>::C;
+  const int64_t n = t.n, nchunks = (n + chunk - 1) / chunk;
+  const int64_t nflags = nchunks + (n + C::BM - 1) / C::BM;  // data flags, then sum flags
+  const unsigned *zeros = nullptr, *one = nullptr;
+  cudaError_t e = flag_sources(&zeros, &one);
+  if (e != cudaSuccess) return e;
+  cudaEvent_t cleared;
+  if ((e = cudaEventCreateWithFlags(&cleared, cudaEventDisableTiming)) != cudaSuccess) return e;
+  const size_t sz = sizeof(T);
+  // flags cleared by the copy engine first; the kernel may only start polling
+  // after that. The kernel is launched BEFORE the chunk copies are enqueued
+  // (enqueueing ~100 copies takes host time that must not delay the compute).
+  e = cudaMemcpyAsync(ready, zeros, nflags * sizeof(unsigned), cudaMemcpyHostToDevice, copy);
+  if (e == cudaSuccess) e = cudaEventRecord(cleared, copy);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(compute, cleared, 0);
+  cudaEventDestroy(cleared);
+  if (e != cudaSuccess) return e;
+  Args2<T> a = make_args<T>(t.W, t.ldw, t.V, t.ldv, t.n_f, t.m, t.n, 1);
+  a.g_row = t.g_row;
+  a.g_col = t.g_col;
+  a.n_v = t.n_v;
+  a.out = static_cast<T*>(t.vals);
+  a.acc = t.acc;
+  a.ready = ready;
+  a.chunk = chunk;
+  a.sums = static_cast<T*>(const_cast<void*>(t.s_row));
+  a.sum_ready = ready + nchunks;
+  if ((e = launch_group<C, kCzek2Streamed>(&a, nullptr, nullptr, 1, compute)) != cudaSuccess)
+    return e;
+  T* dst = static_cast<T*>(const_cast<void*>(t.W));
+  const T* src = static_cast<const T*>(host);
+  for (int64_t c = nchunks - 1; c >= 0; --c) {
+    const int64_t lo = c * chunk, hi = min64(n, lo + chunk);
+    e = host_ld == t.ldw  // same pitch: the chunk is one contiguous span
+            ? cudaMemcpyAsync(dst + lo * t.ldw, src + lo * host_ld, (hi - lo) * t.ldw * sz,
+                              cudaMemcpyHostToDevice, copy)
+            : cudaMemcpy2DAsync(dst + lo * t.ldw, t.ldw * sz, src + lo * host_ld, host_ld * sz,
+                                t.n_f * sz, hi - lo, cudaMemcpyHostToDevice, copy);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(ready + c, one, sizeof(unsigned), cudaMemcpyHostToDevice, copy);
+    if (e != cudaSuccess) {
+      // the launched kernel would wait for chunks that never come: release all
+      // flags so it finishes (its results are discarded by the error)
+      for (int64_t k = 0; k < nflags; ++k)
+        cudaMemcpyAsync(ready + k, one, sizeof(unsigned), cudaMemcpyHostToDevice, copy);
+      return e;
+    }
+  }
+  return cudaSuccess;
+}
+
+cudaError_t czek2_streamed(int dtype, const Czek2Block& t, const void* host, int64_t host_ld,
+                           int64_t chunk, unsigned* ready, cudaStream_t compute,
+                           cudaStream_t copy) {
+  return dtype == kF64
+             ? czek2_streamed_t<double>(t, host, host_ld, chunk, ready, compute, copy)
+             : czek2_streamed_t<float>(t, host, host_ld, chunk, ready, compute, copy);
 }
 
 template <typename T>

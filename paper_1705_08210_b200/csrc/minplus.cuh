@@ -265,16 +265,22 @@ __device__ __forceinline__ int thread_tx() {
 
 // Full-depth mainloop for one tile. `W` / `V` point at the first vector of
 // the tile's rows / columns. All threads of the CTA must call it.
-template <class C, bool PIVOT>
+// SUMS: thread t < BM + BN also folds the column sum of tile vector t (rows,
+// then columns) from the staged chunks -- sequential ascending q from +0,
+// the order of k_colsum, so the sum is bit-identical -- into *vsum.
+template <class C, bool PIVOT, bool SUMS = false>
 __device__ __forceinline__ void minplus_tile(const typename C::T* __restrict__ W, int64_t ldw,
                                              int rows, const typename C::T* __restrict__ V,
                                              int64_t ldv, int cols,
                                              const typename C::T* __restrict__ xj, int64_t n_f,
                                              typename C::T (&acc)[C::TM][C::TN],
-                                             typename C::T* smem) {
+                                             typename C::T* smem,
+                                             typename C::T* vsum = nullptr) {
   using T = typename C::T;
+  using V4 = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
   constexpr int S = C::STAGES;
   const int ty = thread_ty(), tx = thread_tx();
+  T vs = T();
 #pragma unroll
   for (int m = 0; m < C::TM; ++m)
 #pragma unroll
@@ -307,12 +313,29 @@ __device__ __forceinline__ void minplus_tile(const typename C::T* __restrict__ W
       if (PIVOT) pivot_load<C>(smem + (nk % S) * C::STAGE_ELEMS, xj, n_f, nk);
     }
     cp_async_commit();
+    if constexpr (SUMS) {
+      if (threadIdx.x < C::BM + C::BN) {
+        // LDS.128: 8 consecutive threads read 8 rows' 16 B at a 144-B pitch = distinct banks
+        const V4* p = reinterpret_cast<const V4*>(st + threadIdx.x * C::PITCH);
+#pragma unroll
+        for (int h = 0; h < C::BK / C::VEC; ++h) {
+          const V4 x = p[h];
+          if constexpr (sizeof(T) == 8) {
+            vs = Traits<T>::add(Traits<T>::add(vs, x.x), x.y);
+          } else {
+            vs = Traits<T>::add(
+                Traits<T>::add(Traits<T>::add(Traits<T>::add(vs, x.x), x.y), x.z), x.w);
+          }
+        }
+      }
+    }
     const T* As = st;
     const T* Bs = st + C::BM * C::PITCH;
 #pragma unroll
     for (int kk = 0; kk < C::BK; kk += C::VEC) micro_step<C>(acc, As, Bs, ty, tx, kk);
   }
   cp_async_wait<0>();
+  if constexpr (SUMS) *vsum = vs;
 }
 
 // First column tile of row-tile b in a diagonal task (the tile holding

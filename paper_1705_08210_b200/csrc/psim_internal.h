@@ -36,6 +36,11 @@ cudaError_t quantize_bytes(int dtype, const void* vals, int64_t count, void* out
                            cudaStream_t st);
 
 cudaError_t czek2_block(int dtype, const Czek2Block& t, cudaStream_t st);
+cudaError_t czek2_streamed(int dtype, const Czek2Block& t, const void* host, int64_t host_ld,
+                           int64_t chunk, unsigned* ready, cudaStream_t compute,
+                           cudaStream_t copy);
+cudaError_t stream_stats(unsigned long long* out4, int reset);
+constexpr int64_t kStreamMaxFlags = 65536;  // data + sum flags of a streamed run
 // Sorenson (0/1) path: bit packing and the AND+POPC 2-way task (sorenson.cu).
 cudaError_t pack_bits(int dtype, const void* V, int64_t n_fp, int64_t n_vp, int64_t ld,
                       uint32_t* words, int64_t ldw, unsigned long long* flags, cudaStream_t st);

@@ -386,3 +386,78 @@ def test_data_errors_on_device():
     m[1, 2] = np.nan
     with pytest.raises(P.DataError):
         P.run_2way(P.Problem(2, 4, 4, ArraySource(m)), P.DecompGrid())
+
+
+def _pinned_matrix(V):
+    """V (n_f, n_v) copied into page-locked host memory, returned as a Fortran
+    view of it (what a caller staging its data in pinned buffers hands over)."""
+    import torch
+
+    t = torch.empty((V.shape[1], V.shape[0]), dtype=torch.from_numpy(V[:1, :1].copy()).dtype,
+                    pin_memory=True)
+    t.numpy()[:] = V.T
+    return t, t.numpy().T
+
+
+@pytest.mark.parametrize("precision,n_f,n_v", [("double", 777, 1000), ("single", 300, 2500),
+                                               ("double", 33, 5), ("double", 1, 300)])
+def test_streamed_pinned_input_equals_plain_run(precision, n_f, n_v):
+    """A pinned host source takes psim_czek2_streamed (chunked upload overlapped
+    with the kernel, sums folded in the mainloop): values, checksum and
+    degenerate flags equal the oracle's, with device or zero-copy host output."""
+    from oracle import propsim_np as O
+
+    P = _api()
+    dt = np.float64 if precision == "double" else np.float32
+    V = O.uniform(3, n_f, n_v, dt)
+    V[:, 7 % n_v] = 0  # a zero vector: degenerate pairs with itself only if two zero vectors
+    V[:, 11 % n_v] = 0
+    keep, M = _pinned_matrix(V)
+    prob = P.Problem(2, n_f, n_v, ArraySource(M), precision)
+    vals, zero = O.values_2way(V)
+    for host_values in (False, True):
+        res = P.run_2way(prob, P.DecompGrid(), host_values=host_values)
+        got = res.records.values
+        assert (got.view(np.uint64 if dt == np.float64 else np.uint32)
+                == vals.view(np.uint64 if dt == np.float64 else np.uint32)).all()
+        assert res.checksum.hex == O.checksum_hex(np.arange(len(vals)), vals)
+        assert res.degenerate_count == int(zero.sum())
+    del keep
+
+
+def test_streamed_pinned_input_rejects_bad_data():
+    P = _api()
+    V = np.asfortranarray(np.random.default_rng(0).random((64, 300)))
+    V[5, 200] = np.nan
+    keep, M = _pinned_matrix(V)
+    with pytest.raises(P.DataError):
+        P.run_2way(P.Problem(2, 64, 300, ArraySource(M), "double"), P.DecompGrid())
+    M[5, 200] = -1.0
+    with pytest.raises(P.DataError):
+        P.run_2way(P.Problem(2, 64, 300, ArraySource(M), "double"), P.DecompGrid())
+    del keep
+
+
+def test_streamed_capi_validation():
+    import ctypes as C
+
+    import torch
+
+    from paper_1705_08210_b200 import _native as N
+
+    lib = N.lib()
+    dev = torch.empty((10, 32), dtype=torch.float64, device="cuda")
+    acc = torch.zeros(3, dtype=torch.int64, device="cuda")
+    ready = torch.zeros(4, dtype=torch.int32, device="cuda")
+    pageable = np.zeros((10, 32))
+    sums = torch.empty(10, dtype=torch.float64, device="cuda")
+    t = N.Block2(W=dev.data_ptr(), ldw=32, V=dev.data_ptr(), ldv=32, n_f=20, m=10, n=10,
+                 diagonal=1, n_v=10, acc=acc.data_ptr(), s_row=sums.data_ptr())
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    rc = lib.psim_czek2_streamed(N.F64, C.byref(t), pageable.ctypes.data, 20, 4,
+                                 ready.data_ptr(), s1.cuda_stream, s2.cuda_stream)
+    assert rc == 1 and b"pinned" in lib.psim_last_error()
+    t.diagonal = 0
+    rc = lib.psim_czek2_streamed(N.F64, C.byref(t), pageable.ctypes.data, 20, 4,
+                                 ready.data_ptr(), s1.cuda_stream, s2.cuda_stream)
+    assert rc == 1

@@ -3,6 +3,8 @@
 //   v1  pivot min on the landed stage by the whole CTA + a second barrier (production)
 //   v2  each warp rewrites only the A rows it reads (idempotent; warp pairs that
 //       share rows both do it), __syncwarp instead of the second CTA barrier
+//   v3  product minplus_tile with the in-mainloop column sums (SUMS)
+//   v4  product minplus_tile without them
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Xptxas -v \
 //          -I include -I paper_1705_08210_b200/csrc tools/exp_pivot.cu -o build/exp_pivot
 // Run:   build/exp_pivot [n] [n_f]
@@ -90,8 +92,18 @@ __global__ void __launch_bounds__(kNT, C::MINB)
   const int rows = (int)min64(C::BM, n - row0), cols = (int)min64(C::BN, n - col0);
   double acc[C::TM][C::TN];
   const double* xj = W + ((bi * 7 + bj) % n) * ld;  // some pivot vector
-  tile_v<C, VARIANT>(W + row0 * ld, ld, rows, W + col0 * ld, ld, cols, xj, n_f, acc, smem);
   double s = 0;
+  if (VARIANT == 3) {
+    double vs;
+    minplus_tile<C, false, true>(W + row0 * ld, ld, rows, W + col0 * ld, ld, cols, nullptr, n_f,
+                                 acc, smem, &vs);
+    s = vs;
+  } else if (VARIANT == 4) {
+    minplus_tile<C, false>(W + row0 * ld, ld, rows, W + col0 * ld, ld, cols, nullptr, n_f, acc,
+                           smem);
+  } else {
+    tile_v<C, VARIANT>(W + row0 * ld, ld, rows, W + col0 * ld, ld, cols, xj, n_f, acc, smem);
+  }
 #pragma unroll
   for (int m = 0; m < C::TM; ++m)
 #pragma unroll
@@ -156,5 +168,9 @@ int main(int argc, char** argv) {
   run<0>(W, ld, n, nf, out);
   run<1>(W, ld, n, nf, out);
   run<2>(W, ld, n, nf, out);
+  run<3>(W, ld, n, nf, out);
+  run<4>(W, ld, n, nf, out);
+  run<3>(W, ld, n, nf, out);
+  run<4>(W, ld, n, nf, out);
   return 0;
 }
