@@ -6,6 +6,7 @@
 #include <cstring>
 #include <vector>
 
+#include "box3_plan.cuh"
 #include "psim_internal.h"
 
 namespace {
@@ -51,24 +52,23 @@ int check_operand(int dtype, const void* p, int64_t ld, int64_t n_f, const char*
   return PSIM_OK;
 }
 
-// Per-pivot tile and output counts of a 3-way box (see psim_box3_t).
+// Per-pivot tile and output counts of a 3-way box (see psim_box3_t);
+// *n_packed = CTAs of the packed-pair grid (box3_plan.cuh).
 void box3_counts(int dtype, const psim_box3_t& b, std::vector<int64_t>* tile_pref,
-                 std::vector<int64_t>* out_pref) {
+                 std::vector<int64_t>* out_pref, int64_t* n_packed = nullptr) {
   int bm = 0, bn = 0;
   psim::tile_shape(dtype, &bm, &bn);
   const int64_t nJ = b.j1 > b.j0 ? b.j1 - b.j0 : 0;
   tile_pref->assign(nJ + 1, 0);
   out_pref->assign(nJ + 1, 0);
+  int64_t packed = 0;
   for (int64_t jj = 0; jj < nJ; ++jj) {
-    const int64_t j = b.j0 + jj;
-    const int64_t ihi = b.i1 < j ? b.i1 : j;
-    const int64_t klo = b.k0 > j + 1 ? b.k0 : j + 1;
-    const int64_t r = ihi > b.i0 ? ihi - b.i0 : 0;
-    const int64_t c = b.k1 > klo ? b.k1 - klo : 0;
-    const int64_t t = ((r + bm - 1) / bm) * ((c + bn - 1) / bn);
-    (*tile_pref)[jj + 1] = (*tile_pref)[jj] + (r && c ? t : 0);
-    (*out_pref)[jj + 1] = (*out_pref)[jj] + r * c;
+    const psim::Pivot3 g = psim::pivot3(b.i0, b.i1, b.j0, b.j1, b.k0, b.k1, bm, bn, b.j0 + jj);
+    (*tile_pref)[jj + 1] = (*tile_pref)[jj] + g.tiles;
+    (*out_pref)[jj + 1] = (*out_pref)[jj] + g.nrows * g.ncols;
+    packed += g.packed;
   }
+  if (n_packed) *n_packed = packed;
 }
 
 }  // namespace
@@ -285,9 +285,10 @@ int psim_box3_plan(int dtype, const psim_box3_t* box, int64_t* n_out, int64_t* n
   if (int r = check_dtype(dtype)) return r;
   if (!box) return fail(PSIM_ECONFIG, "box is NULL");
   std::vector<int64_t> tp, op;
-  box3_counts(dtype, *box, &tp, &op);
+  int64_t packed = 0;
+  box3_counts(dtype, *box, &tp, &op, &packed);
   if (n_out) *n_out = op.back();
-  if (n_tiles) *n_tiles = tp.back();
+  if (n_tiles) *n_tiles = tp.back() + packed;
   return PSIM_OK;
 }
 
@@ -309,15 +310,16 @@ static int check_box(int dtype, const psim_box3_t* b, bool tables) {
 // mode 0: fused values (psim_czek3_box); 1: raw n_ijk (psim_czek3_box_numerators)
 static int run_box(int dtype, const psim_box3_t* b, int mode, void* stream, const char* what) {
   std::vector<int64_t> tp, op;
-  box3_counts(dtype, *b, &tp, &op);
-  const int64_t n_tiles = tp.back();
-  if (n_tiles == 0) return PSIM_OK;
+  int64_t n_packed = 0;
+  box3_counts(dtype, *b, &tp, &op, &n_packed);
+  const int64_t n_single = tp.back();
+  if (n_single + n_packed == 0) return PSIM_OK;
   cudaStream_t st = S(stream);
   int64_t* d = nullptr;
-  cudaError_t e = cudaMallocAsync(&d, 2 * tp.size() * sizeof(int64_t), st);
+  cudaError_t e = cudaMallocAsync(&d, 3 * tp.size() * sizeof(int64_t), st);
   if (e != cudaSuccess) return cuda_status(e, what);
-  e = mode ? psim::czek3_box_numerators(dtype, *b, d, n_tiles, st)
-           : psim::czek3_box(dtype, *b, d, n_tiles, st);
+  e = mode ? psim::czek3_box_numerators(dtype, *b, d, n_single, n_packed, st)
+           : psim::czek3_box(dtype, *b, d, n_single, n_packed, st);
   cudaError_t e2 = cudaFreeAsync(d, st);
   if (e == cudaSuccess) e = e2;
   return cuda_status(e, what);
@@ -346,7 +348,7 @@ int psim_czek3_from_numerators(int dtype, const psim_box3_t* b, const void* n3, 
   if (e1 == e0) return PSIM_OK;
   cudaStream_t st = S(stream);
   int64_t* d = nullptr;
-  cudaError_t e = cudaMallocAsync(&d, 2 * tp.size() * sizeof(int64_t), st);
+  cudaError_t e = cudaMallocAsync(&d, 3 * tp.size() * sizeof(int64_t), st);
   if (e != cudaSuccess) return cuda_status(e, "psim_czek3_from_numerators workspace");
   e = psim::czek3_from_num(dtype, *b, d, n3, e0, e1, vals, st);
   cudaError_t e2 = cudaFreeAsync(d, st);

@@ -22,6 +22,7 @@
 //
 // Output layout ("pivot-major"): for j in J, the rectangle rows i, columns k
 // row-major, at out_pref[j - j0].
+#include "box3_plan.cuh"
 #include "minplus.cuh"
 #include "psim_internal.h"
 
@@ -44,46 +45,213 @@ __device__ __forceinline__ T czek3_value(const Czek3Box& b, int64_t ai, int64_t 
   return zero ? T(0) : Traits<T>::div(Traits<T>::mul(T(1.5), n3), d);
 }
 
-// One CTA's tile of a box: pivot j (index lo in the box's J range), the
-// tile's rows / cols, and their local columns in blocks A / C.
+// One CTA's tile: up to two row segments and two column segments, each with
+// its own pivot on the segmented side (side 0: rows carry the pivot, the
+// columns are one segment; side 1: columns carry it). A single-pivot tile is
+// one row segment and one column segment.
 struct Tile3 {
-  int64_t lo, j, ncols, r0, c0, ia, kc, jb;
-  int rows, cols;
+  int64_t p0, p1;      // pivots (global) of segment 0 / 1
+  int64_t row0, row1;  // first global row of each row segment
+  int64_t col0, col1;  // first global column of each column segment
+  int nr0, nr1;        // row segment sizes (nr1 may be 0)
+  int nc0, nc1;        // column segment sizes (nc1 may be 0)
+  int side;            // 0: pivot per row segment, 1: pivot per column segment
 };
 
-// tile_pref is read with volatile loads (ld_pref) so the second decode after
-// the mainloop is recomputed, not kept live in registers across it.
-template <class C>
-__device__ __forceinline__ Tile3 decode3(const Czek3Box& b, const int64_t* tile_pref, int64_t nJ) {
-  Tile3 d;
-  // locate pivot j: largest lo with tile_pref[lo] <= blockIdx.x
+// Decode CTA blockIdx.x of a box (tile_pref: per-pivot CTA prefix from
+// box3_plan's pivot3; read with volatile loads so the decode after the
+// mainloop is recomputed rather than held live across it).
+template <class C, bool PACKED>
+__device__ __forceinline__ Tile3 decode3(const Czek3Box& b, const int64_t* tile_pref,
+                                         int64_t nJ) {
+  constexpr int BM = C::BM, BN = C::BN;
   const int64_t t = blockIdx.x;
-  int64_t lo = 0, hi = nJ;  // invariant tile_pref[lo] <= t < tile_pref[hi]
+  int64_t lo = 0, hi = nJ;  // largest lo with tile_pref[lo] <= t
   while (hi - lo > 1) {
     const int64_t mid = (lo + hi) >> 1;
     if (ld_pref(tile_pref + mid) <= t) lo = mid; else hi = mid;
   }
-  d.lo = lo;
-  d.j = b.j0 + lo;
-  const int64_t ihi = min64(b.i1, d.j);
-  const int64_t klo = max64(b.k0, d.j + 1);
-  const int64_t nrows = ihi - b.i0;
-  d.ncols = b.k1 - klo;
-  const int64_t tiles_k = (d.ncols + C::BN - 1) / C::BN;
-  const int64_t lt = t - ld_pref(tile_pref + lo);
-  const int64_t ti = lt / tiles_k, tk = lt - ti * tiles_k;
-  d.r0 = ti * C::BM;
-  d.c0 = tk * C::BN;
-  d.rows = (int)min64(C::BM, nrows - d.r0);
-  d.cols = (int)min64(C::BN, d.ncols - d.c0);
-  d.ia = b.i0 - b.a0 + d.r0;   // local column of the tile's first i in block A
-  d.kc = klo - b.c0 + d.c0;    // local column of the tile's first k in block C
-  d.jb = d.j - b.b0;           // local column of j in block B
+  const int64_t j = b.j0 + lo;
+  int64_t l = t - ld_pref(tile_pref + lo);
+  const Pivot3 g = pivot3(b.i0, b.i1, b.j0, b.j1, b.k0, b.k1, BM, BN, j);
+  Tile3 d;
+  d.p0 = d.p1 = j;
+  d.nr1 = d.nc1 = 0;
+  d.row1 = d.col1 = 0;
+  d.side = 0;
+  if (g.mate < 0) {  // single pivot: row tiles from i0, column tiles from klo
+    const int64_t tiles_k = (g.ncols + BN - 1) / BN;
+    const int64_t ti = l / tiles_k, tk = l - ti * tiles_k;
+    d.row0 = b.i0 + ti * BM;
+    d.col0 = g.klo + tk * BN;
+    d.nr0 = (int)min64(BM, g.nrows - ti * BM);
+    d.nc0 = (int)min64(BN, g.ncols - tk * BN);
+    return d;
+  }
+  Pivot3 h;
+  pivot3_geom(b.i0, b.i1, b.k0, b.k1, BM, BN, g.mate, h);
+  const int64_t q = g.mate;
+  auto clean_col = [&](int64_t ci, Tile3& x) {  // clean column tile Cc + ci
+    x.col0 = b.k0 + (g.Cc + ci) * BN;
+    x.nc0 = (int)min64(BN, b.k1 - x.col0);
+  };
+  if (!PACKED) {
+    const int64_t nAB = 2 * g.R * g.Kc;
+    if (l < nAB) {  // full tiles of j and q, interleaved (same panels)
+      d.p0 = (l & 1) ? q : j;
+      const int64_t rc = l >> 1, ri = rc / g.Kc;
+      d.row0 = b.i0 + ri * BM;
+      d.nr0 = BM;
+      clean_col(rc - ri * g.Kc, d);
+      return d;
+    }
+    l -= nAB;
+    const bool e_j = g.r > 0 && g.w > 0;
+    const bool own = (l == 0 && e_j);  // corner of j, else of q
+    const Pivot3& x = own ? g : h;
+    d.p0 = own ? j : q;
+    d.row0 = b.i0 + g.R * BM;
+    d.nr0 = (int)x.r;
+    d.col0 = x.klo;
+    d.nc0 = (int)x.w;
+    return d;
+  }
+  const int64_t nC = g.r + h.r > 0 ? g.Kc : 0;
+  if (l < nC) {  // ragged rows of both pivots in one tile
+    d.p1 = q;
+    d.row0 = d.row1 = b.i0 + g.R * BM;
+    d.nr0 = (int)g.r;
+    d.nr1 = (int)h.r;
+    clean_col(l, d);
+    return d;
+  }
+  l -= nC;
+  const int64_t nD = g.w + h.w > 0 ? g.R : 0;
+  {  // ragged leading columns of both pivots in one tile (l < nD)
+    d.side = 1;
+    d.p1 = q;
+    d.row0 = b.i0 + l * BM;
+    d.nr0 = BM;
+    d.col0 = g.klo;
+    d.nc0 = (int)g.w;
+    d.col1 = h.klo;
+    d.nc1 = (int)h.w;
+  }
   return d;
 }
 
+// The 3-way mainloop of one (possibly packed) tile: the 2-way pipeline with
+// the pivot min applied to each landed stage. Each thread stages the same
+// A rows (tid/8 + 32r) and B columns every stage, so their sources are
+// resolved once: vector offsets (-1 = zero-fill) into VA / VC, and for the
+// pivot-min the pivot slot each of its staged rows takes.
+template <class C>
+__device__ __forceinline__ void minplus_tile3(const Czek3Box& b, const Tile3& d,
+                                              typename C::T (&acc)[C::TM][C::TN],
+                                              typename C::T* smem) {
+  using T = typename C::T;
+  using V4 = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
+  constexpr int S = C::STAGES, RA = (C::BM * 8) / kNT, RB = (C::BN * 8) / kNT;
+  constexpr int XS = (C::BM + C::BN) * C::PITCH;
+  const int tid = threadIdx.x, ch = tid & 7, r8 = tid >> 3;
+  const int ty = thread_ty(), tx = thread_tx();
+  const T* VA = static_cast<const T*>(b.VA);
+  const T* VC = static_cast<const T*>(b.VC);
+  const T* xsrc = static_cast<const T*>(b.VB) + ((tid >> 3) ? d.p1 : d.p0) * 0;  // set below
+  int a_off[RA], b_off[RB];
+  unsigned a_slot = 0, b_slot = 0;  // bit r: staged row r takes pivot slot 1
+#pragma unroll
+  for (int r = 0; r < RA; ++r) {
+    const int row = r8 + 32 * r;
+    a_off[r] = row < d.nr0 ? (int)(d.row0 - b.a0) + row
+             : row < d.nr0 + d.nr1 ? (int)(d.row1 - b.a0) + row - d.nr0 : -1;
+    if (!d.side && row >= d.nr0) a_slot |= 1u << r;
+  }
+#pragma unroll
+  for (int r = 0; r < RB; ++r) {
+    const int col = r8 + 32 * r;
+    b_off[r] = col < d.nc0 ? (int)(d.col0 - b.c0) + col
+             : col < d.nc0 + d.nc1 ? (int)(d.col1 - b.c0) + col - d.nc0 : -1;
+    if (d.side && col >= d.nc0) b_slot |= 1u << r;
+  }
+  // threads 0-7 stage pivot segment 0, 8-15 segment 1
+  xsrc = static_cast<const T*>(b.VB) + ((tid >= 8 ? d.p1 : d.p0) - b.b0) * b.ldB;
+  const int side = d.side;
+  const int64_t ldA = b.ldA, ldC = b.ldC, n_f = b.n_f;
+
+  auto load = [&](T* st, int kt) {
+    const int64_t q0 = (int64_t)kt * C::BK + ch * C::VEC;
+    const int64_t rem = (n_f - q0) * (int64_t)sizeof(T);
+    const int full = rem >= 16 ? 16 : (rem > 0 ? (int)rem : 0);
+#pragma unroll
+    for (int r = 0; r < RA; ++r) {
+      const int bytes = a_off[r] >= 0 ? full : 0;
+      cp_async16(st + (r8 + 32 * r) * C::PITCH + ch * C::VEC,
+                 bytes ? VA + a_off[r] * ldA + q0 : VA, bytes);
+    }
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      const int bytes = b_off[r] >= 0 ? full : 0;
+      cp_async16(st + (C::BM + r8 + 32 * r) * C::PITCH + ch * C::VEC,
+                 bytes ? VC + b_off[r] * ldC + q0 : VC, bytes);
+    }
+    if (tid < 16) cp_async16(st + XS + (tid >> 3) * C::BK + ch * C::VEC, full ? xsrc + q0 : xsrc,
+                             full);
+  };
+
+#pragma unroll
+  for (int m = 0; m < C::TM; ++m)
+#pragma unroll
+    for (int n = 0; n < C::TN; ++n) acc[m][n] = T(0);
+  const int KT = (int)((n_f + C::BK - 1) / C::BK);
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) {
+    if (s < KT) load(smem + s * C::STAGE_ELEMS, s);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<S - 2>();
+    __syncthreads();
+    T* st = smem + (kt % S) * C::STAGE_ELEMS;
+    {  // pivot min on the segmented side, each staged row with its own slot
+      T* base = st + (side ? C::BM * C::PITCH : 0);
+      const unsigned slots = side ? b_slot : a_slot;
+      constexpr int RR = RA > RB ? RA : RB;
+#pragma unroll
+      for (int r = 0; r < RR; ++r) {
+        if (r >= (side ? RB : RA)) break;
+        const V4 x = *reinterpret_cast<const V4*>(st + XS + ((slots >> r) & 1u) * C::BK +
+                                                  ch * C::VEC);
+        V4* p = reinterpret_cast<V4*>(base + (r8 + 32 * r) * C::PITCH + ch * C::VEC);
+        V4 a = *p;
+        if constexpr (sizeof(T) == 8) {
+          a.x = Traits<double>::min(x.x, a.x);
+          a.y = Traits<double>::min(x.y, a.y);
+        } else {
+          a.x = Traits<float>::min(x.x, a.x);
+          a.y = Traits<float>::min(x.y, a.y);
+          a.z = Traits<float>::min(x.z, a.z);
+          a.w = Traits<float>::min(x.w, a.w);
+        }
+        *p = a;
+      }
+    }
+    __syncthreads();
+    const int nk = kt + S - 1;
+    if (nk < KT) load(smem + (nk % S) * C::STAGE_ELEMS, nk);
+    cp_async_commit();
+    const T* As = st;
+    const T* Bs = st + C::BM * C::PITCH;
+#pragma unroll
+    for (int kk = 0; kk < C::BK; kk += C::VEC) micro_step<C>(acc, As, Bs, ty, tx, kk);
+  }
+  cp_async_wait<0>();
+}
+
 // RAW = true writes the n_ijk partial sums (field-split path) instead of values.
-template <class C, bool RAW>
+// PACKED selects the grid of two-pivot tiles (its own launch, so each grid
+// runs a single mainloop body).
+template <class C, bool RAW, bool PACKED>
 __global__ void __launch_bounds__(kNT, C::MINB)
     k_czek3(const Czek3Box b, const int64_t* __restrict__ tile_pref,
             const int64_t* __restrict__ out_pref, int64_t nJ) {
@@ -93,62 +261,56 @@ __global__ void __launch_bounds__(kNT, C::MINB)
 
   T acc[C::TM][C::TN];
   {
-    const Tile3 d = decode3<C>(b, tile_pref, nJ);
-    minplus_tile<C, true>(static_cast<const T*>(b.VA) + d.ia * b.ldA, b.ldA, d.rows,
-                          static_cast<const T*>(b.VC) + d.kc * b.ldC, b.ldC, d.cols,
-                          static_cast<const T*>(b.VB) + d.jb * b.ldB, b.n_f, acc, smem);
+    const Tile3 d = decode3<C, PACKED>(b, tile_pref, nJ);
+    if (PACKED) {  // segmented staging, per-segment pivot
+      minplus_tile3<C>(b, d, acc, smem);
+    } else {  // one pivot: the lean loop (measured 5% faster than the segmented one)
+      minplus_tile<C, true>(static_cast<const T*>(b.VA) + (d.row0 - b.a0) * b.ldA, b.ldA, d.nr0,
+                            static_cast<const T*>(b.VC) + (d.col0 - b.c0) * b.ldC, b.ldC, d.nc0,
+                            static_cast<const T*>(b.VB) + (d.p0 - b.b0) * b.ldB, b.n_f, acc,
+                            smem);
+    }
   }
   // decoded again (measured: keeping the tile state live across the mainloop
   // costs registers and ~4% of the mainloop's issue rate)
-  const Tile3 d = decode3<C>(b, tile_pref, nJ);
-  const int64_t lo = d.lo, j = d.j, ncols = d.ncols, r0 = d.r0, c0 = d.c0;
-  const int64_t ia = d.ia, kc = d.kc, jb = d.jb;
-  const int rows = d.rows, cols = d.cols;
+  const Tile3 d = decode3<C, PACKED>(b, tile_pref, nJ);
 
   T* out = static_cast<T*>(b.vals);
-  const int64_t obase = out_pref[lo];
   const uint64_t nv = (uint64_t)b.n_v;
-
   const int ty = thread_ty(), tx = thread_tx();
-  if (RAW) {
-#pragma unroll
-    for (int mi = 0; mi < C::TM; ++mi) {
-      const int li = ty + 16 * mi;
-      if (li >= rows) continue;
-      const int64_t orow = obase + (r0 + li) * ncols + c0;
-#pragma unroll
-      for (int nk = 0; nk < C::TN; ++nk) {
-        const int lk = tx + 16 * nk;
-        if (lk < cols) out[orow + lk] = acc[mi][nk];
-      }
-    }
-    return;
-  }
   Cks c;
 #pragma unroll
   for (int mi = 0; mi < C::TM; ++mi) {
     const int li = ty + 16 * mi;
-    if (li >= rows) continue;
-    const int64_t ai = ia + li;            // local in A
-    const int64_t i = b.a0 + ai;           // global
-    // triple_index(i, j, k) = base_ij + (k - j - 1), base_ij = C3(n)-C3(n-i)+pair_index(j-i-1, j-i, n-i-1)
-    const uint64_t base_ij = choose3(nv) - choose3(nv - (uint64_t)i) +
-                             pair_index((uint64_t)(j - i - 1), (uint64_t)(j - i), nv - (uint64_t)i - 1);
-    const int64_t orow = obase + (r0 + li) * ncols + c0;
+    if (li >= d.nr0 + d.nr1) continue;
+    const bool rs = li >= d.nr0;
+    const int64_t i = rs ? d.row1 + (li - d.nr0) : d.row0 + li;  // global row
 #pragma unroll
     for (int nk = 0; nk < C::TN; ++nk) {
       const int lk = tx + 16 * nk;
-      if (lk >= cols) continue;
-      const int64_t kcl = kc + lk;          // local in C
-      const int64_t k = b.c0 + kcl;         // global
+      if (lk >= d.nc0 + d.nc1) continue;
+      const bool cs = lk >= d.nc0;
+      const int64_t k = cs ? d.col1 + (lk - d.nc0) : d.col0 + lk;  // global column
+      const int64_t j = (d.side ? cs : rs) ? d.p1 : d.p0;
+      // pivot-major position: out_pref[j - j0] + (i - i0) * ncols(j) + (k - klo(j))
+      const int64_t klo = max64(b.k0, j + 1);
+      const int64_t pos = out_pref[j - b.j0] + (i - b.i0) * (b.k1 - klo) + (k - klo);
+      if (RAW) {
+        out[pos] = acc[mi][nk];
+        continue;
+      }
       bool zero;
-      const T v = czek3_value<T>(b, ai, jb, kcl, acc[mi][nk], zero);
-      if (out) out[orow + lk] = v;
+      const T v = czek3_value<T>(b, i - b.a0, j - b.b0, k - b.c0, acc[mi][nk], zero);
+      if (out) out[pos] = v;
+      // triple_index(i, j, k) = C3(n)-C3(n-i) + pair_index(j-i-1, k-i-1, n-i-1)
+      const uint64_t base_ij = choose3(nv) - choose3(nv - (uint64_t)i) +
+                               pair_index((uint64_t)(j - i - 1), (uint64_t)(j - i),
+                                          nv - (uint64_t)i - 1);
       c.term(base_ij + (uint64_t)(k - j - 1), Traits<T>::bits(v));
       c.deg += zero ? 1ull : 0ull;
     }
   }
-  cks_block_flush<kNT>(b.acc, c);
+  if (!RAW) cks_block_flush<kNT>(b.acc, c);
 }
 
 // Values + checksum for elements [e0, e1) of a box's pivot-major layout from
@@ -183,70 +345,73 @@ __global__ void __launch_bounds__(256) k_czek3_from_num(const Czek3Box b,
   cks_block_flush<256>(b.acc, c);
 }
 
-// Per-pivot prefix sums of CTA tiles and output elements for a box, one CTA:
-// each thread folds a contiguous j range, then a block scan of the partials.
+// Per-pivot prefix sums of single-pivot CTAs, output elements and packed
+// CTAs for a box (pivot3), one CTA: each thread folds a contiguous j range,
+// then a block scan of the partials. pref = [tiles | out | packed], nJ+1 each.
 __global__ void __launch_bounds__(1024) k_box3_prefix(int64_t i0, int64_t i1, int64_t j0,
-                                                      int64_t j1, int64_t k0, int64_t k1, int64_t bm, int64_t bn,
-                                                      int64_t* __restrict__ tile_pref,
-                                                      int64_t* __restrict__ out_pref) {
-  __shared__ int64_t s_t[1024], s_o[1024];
+                                                      int64_t j1, int64_t k0, int64_t k1,
+                                                      int64_t bm, int64_t bn,
+                                                      int64_t* __restrict__ pref) {
+  __shared__ int64_t s[3][1024];
   const int64_t nJ = j1 - j0;
   const int64_t per = (nJ + blockDim.x - 1) / blockDim.x;
   const int64_t a = min64(nJ, threadIdx.x * per), e = min64(nJ, a + per);
-  auto counts = [&](int64_t jj, int64_t& t, int64_t& o) {
-    const int64_t j = j0 + jj;
-    const int64_t r = max64(0, min64(i1, j) - i0);
-    const int64_t c = max64(0, k1 - max64(k0, j + 1));
-    t = ((r + bm - 1) / bm) * ((c + bn - 1) / bn);
-    o = r * c;
+  auto counts = [&](int64_t jj, int64_t (&c)[3]) {
+    const Pivot3 g = pivot3(i0, i1, j0, j1, k0, k1, bm, bn, j0 + jj);
+    c[0] = g.tiles;
+    c[1] = g.nrows * g.ncols;
+    c[2] = g.packed;
   };
-  int64_t st = 0, so = 0;
+  int64_t sum[3] = {0, 0, 0};
   for (int64_t jj = a; jj < e; ++jj) {
-    int64_t t, o;
-    counts(jj, t, o);
-    st += t;
-    so += o;
+    int64_t c[3];
+    counts(jj, c);
+    for (int x = 0; x < 3; ++x) sum[x] += c[x];
   }
-  s_t[threadIdx.x] = st;
-  s_o[threadIdx.x] = so;
+  for (int x = 0; x < 3; ++x) s[x][threadIdx.x] = sum[x];
   __syncthreads();
   for (int off = 1; off < (int)blockDim.x; off <<= 1) {  // inclusive Hillis-Steele scan
-    int64_t vt = threadIdx.x >= off ? s_t[threadIdx.x - off] : 0;
-    int64_t vo = threadIdx.x >= off ? s_o[threadIdx.x - off] : 0;
+    int64_t v[3];
+    for (int x = 0; x < 3; ++x) v[x] = threadIdx.x >= off ? s[x][threadIdx.x - off] : 0;
     __syncthreads();
-    s_t[threadIdx.x] += vt;
-    s_o[threadIdx.x] += vo;
+    for (int x = 0; x < 3; ++x) s[x][threadIdx.x] += v[x];
     __syncthreads();
   }
-  int64_t rt = threadIdx.x ? s_t[threadIdx.x - 1] : 0;
-  int64_t ro = threadIdx.x ? s_o[threadIdx.x - 1] : 0;
+  int64_t run[3];
+  for (int x = 0; x < 3; ++x) run[x] = threadIdx.x ? s[x][threadIdx.x - 1] : 0;
   for (int64_t jj = a; jj < e; ++jj) {
-    tile_pref[jj] = rt;
-    out_pref[jj] = ro;
-    int64_t t, o;
-    counts(jj, t, o);
-    rt += t;
-    ro += o;
+    int64_t c[3];
+    counts(jj, c);
+    for (int x = 0; x < 3; ++x) {
+      pref[x * (nJ + 1) + jj] = run[x];
+      run[x] += c[x];
+    }
   }
-  if (threadIdx.x == blockDim.x - 1) {
-    tile_pref[nJ] = s_t[threadIdx.x];
-    out_pref[nJ] = s_o[threadIdx.x];
-  }
+  if (threadIdx.x == blockDim.x - 1)
+    for (int x = 0; x < 3; ++x) pref[x * (nJ + 1) + nJ] = s[x][threadIdx.x];
 }
 
 template <typename T, bool RAW>
-static cudaError_t czek3_t(const Czek3Box& b, int64_t* work, int64_t n_tiles, cudaStream_t st) {
+static cudaError_t czek3_t(const Czek3Box& b, int64_t* work, int64_t n_single, int64_t n_packed,
+                           cudaStream_t st) {
   using C = typename Prod<T>::C;
-  cudaError_t e = cudaFuncSetAttribute(k_czek3<C, RAW>,
+  cudaError_t e = cudaFuncSetAttribute(k_czek3<C, RAW, false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_czek3<C, RAW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::SMEM_BYTES);
   if (e != cudaSuccess) return e;
-  if (n_tiles <= 0) return cudaSuccess;
-  if (n_tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  if (n_single + n_packed <= 0) return cudaSuccess;
+  if (n_single > 0x7fffffffLL || n_packed > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
   const int64_t nJ = b.j1 - b.j0;
   int64_t* tp = work;
   int64_t* op = work + nJ + 1;
-  k_box3_prefix<<<1, 1024, 0, st>>>(b.i0, b.i1, b.j0, b.j1, b.k0, b.k1, C::BM, C::BN, tp, op);
-  k_czek3<C, RAW><<<(unsigned)n_tiles, kNT, C::SMEM_BYTES, st>>>(b, tp, op, nJ);
+  int64_t* pp = work + 2 * (nJ + 1);
+  k_box3_prefix<<<1, 1024, 0, st>>>(b.i0, b.i1, b.j0, b.j1, b.k0, b.k1, C::BM, C::BN, work);
+  if (n_single > 0)
+    k_czek3<C, RAW, false><<<(unsigned)n_single, kNT, C::SMEM_BYTES, st>>>(b, tp, op, nJ);
+  if (n_packed > 0)
+    k_czek3<C, RAW, true><<<(unsigned)n_packed, kNT, C::SMEM_BYTES, st>>>(b, pp, op, nJ);
   return cudaGetLastError();
 }
 
@@ -256,9 +421,8 @@ static cudaError_t czek3_from_num_t(const Czek3Box& b, int64_t* work, const void
   using C = typename Prod<T>::C;
   if (e1 <= e0) return cudaSuccess;
   const int64_t nJ = b.j1 - b.j0;
-  int64_t* tp = work;
   int64_t* op = work + nJ + 1;
-  k_box3_prefix<<<1, 1024, 0, st>>>(b.i0, b.i1, b.j0, b.j1, b.k0, b.k1, C::BM, C::BN, tp, op);
+  k_box3_prefix<<<1, 1024, 0, st>>>(b.i0, b.i1, b.j0, b.j1, b.k0, b.k1, C::BM, C::BN, work);
   int64_t blocks = (e1 - e0 + 255) / 256;
   if (blocks > 148 * 32) blocks = 148 * 32;
   k_czek3_from_num<T><<<(unsigned)blocks, 256, 0, st>>>(b, op, nJ, static_cast<const T*>(n3), e0,
@@ -266,10 +430,10 @@ static cudaError_t czek3_from_num_t(const Czek3Box& b, int64_t* work, const void
   return cudaGetLastError();
 }
 
-cudaError_t czek3_box_numerators(int dtype, const Czek3Box& b, int64_t* d_work, int64_t n_tiles,
-                                 cudaStream_t st) {
-  return dtype == kF64 ? czek3_t<double, true>(b, d_work, n_tiles, st)
-                       : czek3_t<float, true>(b, d_work, n_tiles, st);
+cudaError_t czek3_box_numerators(int dtype, const Czek3Box& b, int64_t* d_work, int64_t n_single,
+                                 int64_t n_packed, cudaStream_t st) {
+  return dtype == kF64 ? czek3_t<double, true>(b, d_work, n_single, n_packed, st)
+                       : czek3_t<float, true>(b, d_work, n_single, n_packed, st);
 }
 
 cudaError_t czek3_from_num(int dtype, const Czek3Box& b, int64_t* d_work, const void* n3,
@@ -288,10 +452,10 @@ void tile_shape(int dtype, int* bm, int* bn) {
   }
 }
 
-cudaError_t czek3_box(int dtype, const Czek3Box& b, int64_t* d_work, int64_t n_tiles,
-                      cudaStream_t st) {
-  return dtype == kF64 ? czek3_t<double, false>(b, d_work, n_tiles, st)
-                       : czek3_t<float, false>(b, d_work, n_tiles, st);
+cudaError_t czek3_box(int dtype, const Czek3Box& b, int64_t* d_work, int64_t n_single,
+                      int64_t n_packed, cudaStream_t st) {
+  return dtype == kF64 ? czek3_t<double, false>(b, d_work, n_single, n_packed, st)
+                       : czek3_t<float, false>(b, d_work, n_single, n_packed, st);
 }
 
 }  // namespace psim

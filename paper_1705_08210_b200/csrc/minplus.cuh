@@ -50,7 +50,7 @@ struct Cfg {
   static constexpr int BK = 128 / (int)sizeof(T);    // q per stage (one 128-B chunk)
   static constexpr int VEC = 16 / (int)sizeof(T);    // q per LDS.128
   static constexpr int PITCH = kPitchBytes / (int)sizeof(T);
-  static constexpr int STAGE_ELEMS = (BM + BN) * PITCH + BK;  // A, B, pivot chunk
+  static constexpr int STAGE_ELEMS = (BM + BN) * PITCH + 2 * BK;  // A, B, 2 pivot chunks
   static constexpr int SMEM_BYTES = STAGES * STAGE_ELEMS * (int)sizeof(T);
   static_assert((BM * 8) % kNT == 0 && (BN * 8) % kNT == 0, "tile / thread mismatch");
   static_assert(sizeof(T) == 8 || TN % 2 == 0, "FP32 pairs columns for FADD2");

@@ -55,13 +55,14 @@ cudaError_t czek2_from_num(int dtype, const void* N, int64_t r0, int64_t r1, int
                            int64_t g_row, int64_t g_col, int64_t n_v, void* vals,
                            unsigned long long* acc, cudaStream_t st);
 
-// Launches the box kernel; the per-pivot tile / output prefix sums are built
-// on the device in `d_work` (2 * (j1 - j0 + 1) int64).
-cudaError_t czek3_box(int dtype, const Czek3Box& b, int64_t* d_work, int64_t n_tiles,
-                      cudaStream_t st);
+// Launches the box kernels (single-pivot grid, then the packed-pair grid,
+// box3_plan.cuh); the per-pivot prefix sums are built on the device in
+// `d_work` (3 * (j1 - j0 + 1) int64).
+cudaError_t czek3_box(int dtype, const Czek3Box& b, int64_t* d_work, int64_t n_single,
+                      int64_t n_packed, cudaStream_t st);
 // Same box, writing the n_ijk partial sums to b.vals instead of values.
-cudaError_t czek3_box_numerators(int dtype, const Czek3Box& b, int64_t* d_work, int64_t n_tiles,
-                                 cudaStream_t st);
+cudaError_t czek3_box_numerators(int dtype, const Czek3Box& b, int64_t* d_work, int64_t n_single,
+                                 int64_t n_packed, cudaStream_t st);
 // Values + checksum of elements [e0, e1) of the box from folded n_ijk.
 cudaError_t czek3_from_num(int dtype, const Czek3Box& b, int64_t* d_work, const void* n3,
                            int64_t e0, int64_t e1, void* vals, cudaStream_t st);
