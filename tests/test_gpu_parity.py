@@ -290,6 +290,39 @@ def test_large_3way_sampled_and_stage_tiling():
     assert parts[0].records.__len__() + parts[1].records.__len__() == len(vals)
 
 
+def test_3way_packed_pair_tiles_sampled():
+    """FP64 boxes pair pivot j with its mate (box3_plan.cuh): the ragged rows
+    [128R, j) and leading columns (j, 128R + 128) of two pivots share one
+    tile. Triples inside one 128-block are exactly those cells; they, plus
+    random ones, must equal the column-only recompute bit for bit, and the
+    checksum must equal the checksum of all returned values."""
+    from oracle import propsim_np as O
+
+    P = _api()
+    n_f, n_v = 700, 384
+    prob = P.Problem(3, n_f, n_v, P.gen_uniform(8, n_f, n_v), "double")
+    res = P.run_3way(prob, P.DecompGrid())
+    vals = res.records.values
+    assert res.checksum.hex == O.checksum_hex(np.arange(len(vals)), vals)
+    rng = np.random.default_rng(17)
+    triples = set(_sample(rng, n_v, 150, 3))
+    while len(triples) < 450:  # i < j < k all inside one 128-block
+        blk = int(rng.integers(0, n_v // 128))
+        t = tuple(sorted(int(x) for x in rng.choice(128, size=3, replace=False) + 128 * blk))
+        triples.add(t)
+    triples = sorted(triples)
+    got = _recompute(P, O, "uniform", 8, n_f, n_v, triples, "double")
+    idx = [P.triple_index(*t, n_v) for t in triples]
+    assert (vals[idx].view(np.uint64) == got.view(np.uint64)).all()
+    # the same triples from a run whose boxes cannot pair (k range not aligned
+    # with i): per-pivot tiling only
+    part = P.run_3way(prob, P.DecompGrid(n_pv=2, n_st=2), stage=1)
+    pv = dict(zip(part.records.canonical_indices.tolist(), part.records.values.tolist()))
+    for t, v in zip(idx, vals[idx]):
+        if t in pv:
+            assert np.float64(pv[t]).view(np.uint64) == np.float64(v).view(np.uint64)
+
+
 def test_large_field_split_sampled():
     """A cfg5-like deep field axis (n_f = 1,000,000 FP64) split over n_pf = 4
     slabs (ordered fold): sampled pairs bitwise vs the per-slab recompute."""
