@@ -189,6 +189,12 @@ int psim_quantize_bytes(int dtype, const void* vals, int64_t count, uint8_t* out
                         unsigned long long* flag, void* stream);
 /* Output element count and CTA-tile count of a 3-way box (host-only, sync). */
 int psim_box3_plan(int dtype, const psim_box3_t* box, int64_t* n_out, int64_t* n_tiles);
+/* The tile CTA t of a box's single-pivot grid (packed = 0) or two-segment
+ * grid (packed = 1) computes, decoded by the kernels' own code (host-only;
+ * the CPU tests check exact coverage with it). out[11] = p0, p1, row0, row1,
+ * col0, col1, nr0, nr1, nc0, nc1, side; *n_grid = CTAs of that grid. */
+int psim_box3_tile(int dtype, const psim_box3_t* box, int packed, int64_t t, int64_t* out,
+                   int64_t* n_grid);
 /* Fused 3-way box (see psim_box3_t). */
 int psim_czek3_box(int dtype, const psim_box3_t* box, void* stream);
 /* Field-axis path of a box (metrics3.py:163-164): n_ijk = sum_q min(min(x_j, v_i), v_k)

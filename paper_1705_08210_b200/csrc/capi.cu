@@ -55,18 +55,21 @@ int check_operand(int dtype, const void* p, int64_t ld, int64_t n_f, const char*
 // Per-pivot tile and output counts of a 3-way box (see psim_box3_t);
 // *n_packed = CTAs of the packed-pair grid (box3_plan.cuh).
 void box3_counts(int dtype, const psim_box3_t& b, std::vector<int64_t>* tile_pref,
-                 std::vector<int64_t>* out_pref, int64_t* n_packed = nullptr) {
+                 std::vector<int64_t>* out_pref, int64_t* n_packed = nullptr,
+                 std::vector<int64_t>* packed_pref = nullptr) {
   int bm = 0, bn = 0;
   psim::tile_shape(dtype, &bm, &bn);
   const int64_t nJ = b.j1 > b.j0 ? b.j1 - b.j0 : 0;
   tile_pref->assign(nJ + 1, 0);
   out_pref->assign(nJ + 1, 0);
   int64_t packed = 0;
+  if (packed_pref) packed_pref->assign(nJ + 1, 0);
   for (int64_t jj = 0; jj < nJ; ++jj) {
     const psim::Pivot3 g = psim::pivot3(b.i0, b.i1, b.j0, b.j1, b.k0, b.k1, bm, bn, b.j0 + jj);
     (*tile_pref)[jj + 1] = (*tile_pref)[jj] + g.tiles;
     (*out_pref)[jj + 1] = (*out_pref)[jj] + g.nrows * g.ncols;
     packed += g.packed;
+    if (packed_pref) (*packed_pref)[jj + 1] = packed;
   }
   if (n_packed) *n_packed = packed;
 }
@@ -289,6 +292,34 @@ int psim_box3_plan(int dtype, const psim_box3_t* box, int64_t* n_out, int64_t* n
   box3_counts(dtype, *box, &tp, &op, &packed);
   if (n_out) *n_out = op.back();
   if (n_tiles) *n_tiles = tp.back() + packed;
+  return PSIM_OK;
+}
+
+int psim_box3_tile(int dtype, const psim_box3_t* box, int packed, int64_t t, int64_t* out,
+                   int64_t* n_grid) {
+  if (int r = check_dtype(dtype)) return r;
+  if (!box || !out) return fail(PSIM_ECONFIG, "box / out is NULL");
+  std::vector<int64_t> tp, op, pp;
+  int64_t np = 0;
+  box3_counts(dtype, *box, &tp, &op, &np, &pp);
+  const std::vector<int64_t>& pref = packed ? pp : tp;
+  if (n_grid) *n_grid = pref.back();
+  if (t < 0 || t >= pref.back()) return fail(PSIM_ECONFIG, "tile %lld outside the grid", (long long)t);
+  const int64_t nJ = box->j1 - box->j0;
+  psim::Tile3 d;
+  int bm = 0, bn = 0;
+  psim::tile_shape(dtype, &bm, &bn);
+  if (bm == 128 && bn == 128)
+    d = packed ? psim::box3_decode<128, 128, true>(*box, pref.data(), nJ, t)
+               : psim::box3_decode<128, 128, false>(*box, pref.data(), nJ, t);
+  else if (bm == 128 && bn == 64)
+    d = packed ? psim::box3_decode<128, 64, true>(*box, pref.data(), nJ, t)
+               : psim::box3_decode<128, 64, false>(*box, pref.data(), nJ, t);
+  else
+    return fail(PSIM_ERUNTIME, "psim_box3_tile: unexpected tile shape %dx%d", bm, bn);
+  const int64_t v[11] = {d.p0, d.p1, d.row0, d.row1, d.col0, d.col1, d.nr0, d.nr1, d.nc0, d.nc1,
+                         d.side};
+  for (int x = 0; x < 11; ++x) out[x] = v[x];
   return PSIM_OK;
 }
 

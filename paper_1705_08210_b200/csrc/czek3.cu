@@ -45,101 +45,6 @@ __device__ __forceinline__ T czek3_value(const Czek3Box& b, int64_t ai, int64_t 
   return zero ? T(0) : Traits<T>::div(Traits<T>::mul(T(1.5), n3), d);
 }
 
-// One CTA's tile: up to two row segments and two column segments, each with
-// its own pivot on the segmented side (side 0: rows carry the pivot, the
-// columns are one segment; side 1: columns carry it). A single-pivot tile is
-// one row segment and one column segment.
-struct Tile3 {
-  int64_t p0, p1;      // pivots (global) of segment 0 / 1
-  int64_t row0, row1;  // first global row of each row segment
-  int64_t col0, col1;  // first global column of each column segment
-  int nr0, nr1;        // row segment sizes (nr1 may be 0)
-  int nc0, nc1;        // column segment sizes (nc1 may be 0)
-  int side;            // 0: pivot per row segment, 1: pivot per column segment
-};
-
-// Decode CTA blockIdx.x of a box (tile_pref: per-pivot CTA prefix from
-// box3_plan's pivot3; read with volatile loads so the decode after the
-// mainloop is recomputed rather than held live across it).
-template <class C, bool PACKED>
-__device__ __forceinline__ Tile3 decode3(const Czek3Box& b, const int64_t* tile_pref,
-                                         int64_t nJ) {
-  constexpr int BM = C::BM, BN = C::BN;
-  const int64_t t = blockIdx.x;
-  int64_t lo = 0, hi = nJ;  // largest lo with tile_pref[lo] <= t
-  while (hi - lo > 1) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (ld_pref(tile_pref + mid) <= t) lo = mid; else hi = mid;
-  }
-  const int64_t j = b.j0 + lo;
-  int64_t l = t - ld_pref(tile_pref + lo);
-  const Pivot3 g = pivot3(b.i0, b.i1, b.j0, b.j1, b.k0, b.k1, BM, BN, j);
-  Tile3 d;
-  d.p0 = d.p1 = j;
-  d.nr1 = d.nc1 = 0;
-  d.row1 = d.col1 = 0;
-  d.side = 0;
-  if (g.mate < 0) {  // single pivot: row tiles from i0, column tiles from klo
-    const int64_t tiles_k = (g.ncols + BN - 1) / BN;
-    const int64_t ti = l / tiles_k, tk = l - ti * tiles_k;
-    d.row0 = b.i0 + ti * BM;
-    d.col0 = g.klo + tk * BN;
-    d.nr0 = (int)min64(BM, g.nrows - ti * BM);
-    d.nc0 = (int)min64(BN, g.ncols - tk * BN);
-    return d;
-  }
-  Pivot3 h;
-  pivot3_geom(b.i0, b.i1, b.k0, b.k1, BM, BN, g.mate, h);
-  const int64_t q = g.mate;
-  auto clean_col = [&](int64_t ci, Tile3& x) {  // clean column tile Cc + ci
-    x.col0 = b.k0 + (g.Cc + ci) * BN;
-    x.nc0 = (int)min64(BN, b.k1 - x.col0);
-  };
-  if (!PACKED) {
-    const int64_t nAB = 2 * g.R * g.Kc;
-    if (l < nAB) {  // full tiles of j and q, interleaved (same panels)
-      d.p0 = (l & 1) ? q : j;
-      const int64_t rc = l >> 1, ri = rc / g.Kc;
-      d.row0 = b.i0 + ri * BM;
-      d.nr0 = BM;
-      clean_col(rc - ri * g.Kc, d);
-      return d;
-    }
-    l -= nAB;
-    const bool e_j = g.r > 0 && g.w > 0;
-    const bool own = (l == 0 && e_j);  // corner of j, else of q
-    const Pivot3& x = own ? g : h;
-    d.p0 = own ? j : q;
-    d.row0 = b.i0 + g.R * BM;
-    d.nr0 = (int)x.r;
-    d.col0 = x.klo;
-    d.nc0 = (int)x.w;
-    return d;
-  }
-  const int64_t nC = g.r + h.r > 0 ? g.Kc : 0;
-  if (l < nC) {  // ragged rows of both pivots in one tile
-    d.p1 = q;
-    d.row0 = d.row1 = b.i0 + g.R * BM;
-    d.nr0 = (int)g.r;
-    d.nr1 = (int)h.r;
-    clean_col(l, d);
-    return d;
-  }
-  l -= nC;
-  const int64_t nD = g.w + h.w > 0 ? g.R : 0;
-  {  // ragged leading columns of both pivots in one tile (l < nD)
-    d.side = 1;
-    d.p1 = q;
-    d.row0 = b.i0 + l * BM;
-    d.nr0 = BM;
-    d.col0 = g.klo;
-    d.nc0 = (int)g.w;
-    d.col1 = h.klo;
-    d.nc1 = (int)h.w;
-  }
-  return d;
-}
-
 // The 3-way mainloop of one (possibly packed) tile: the 2-way pipeline with
 // the pivot min applied to each landed stage. Each thread stages the same
 // A rows (tid/8 + 32r) and B columns every stage, so their sources are
@@ -261,7 +166,7 @@ __global__ void __launch_bounds__(kNT, C::MINB)
 
   T acc[C::TM][C::TN];
   {
-    const Tile3 d = decode3<C, PACKED>(b, tile_pref, nJ);
+    const Tile3 d = box3_decode<C::BM, C::BN, PACKED>(b, tile_pref, nJ, blockIdx.x);
     if (PACKED) {  // segmented staging, per-segment pivot
       minplus_tile3<C>(b, d, acc, smem);
     } else {  // one pivot: the lean loop (measured 5% faster than the segmented one)
@@ -273,7 +178,7 @@ __global__ void __launch_bounds__(kNT, C::MINB)
   }
   // decoded again (measured: keeping the tile state live across the mainloop
   // costs registers and ~4% of the mainloop's issue rate)
-  const Tile3 d = decode3<C, PACKED>(b, tile_pref, nJ);
+  const Tile3 d = box3_decode<C::BM, C::BN, PACKED>(b, tile_pref, nJ, blockIdx.x);
 
   T* out = static_cast<T*>(b.vals);
   const uint64_t nv = (uint64_t)b.n_v;
