@@ -282,6 +282,8 @@ def run_ours(args) -> dict | None:
     runner.teardown()
     if not args.no_e2e and arity == 2:
         e2e = e2e_2way(P, prob, grid, precision, args, total_cmp, world, rank)
+    elif not args.no_e2e and arity == 3:
+        e2e = e2e_3way(P, prob, grid, precision, args, total_cmp, world, rank)
 
     line = None
     if rank == 0:
@@ -392,6 +394,57 @@ def e2e_2way(P, prob, grid, precision, args, total_cmp, world, rank) -> dict:
                             else "row bands in HBM, D2H copies overlapped with the next band"),
             "api": f"paper_1705_08210_b200.run_2way(Problem(2, n_f, n_v, pinned slab source), "
                    f"grid, transport='{transport}', host_values=True)"}
+
+
+def e2e_3way(P, prob, grid, precision, args, total_cmp, world, rank) -> dict:
+    """run_3way through the public API with this rank's input slab in pinned
+    host memory: every step copies the slab H2D (and, under NCCL, circulates
+    the blocks), runs every box, and reads back the checksum words. cfg4's
+    C(6000, 3) values are 288 GB -- more than host memory -- so they stay
+    reduced to the 128-bit checksum on the device (keep_values=False).
+    Wall time per step, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1705_08210_b200 import device as D
+    from paper_1705_08210_b200.domain import coords_of_rank
+
+    coords = coords_of_rank(rank, grid)
+    blk = D.load_block(prob, grid, coords, torch.device("cuda"))
+    host = torch.empty((blk.n_vp, blk.n_fp), dtype=blk.data.dtype, pin_memory=True)
+    host.copy_(blk.data[:, :blk.n_fp])
+    del blk
+    src = SlabSource(host.numpy().T, coords)
+    e2e_prob = P.Problem(3, prob.n_f, prob.n_v, src, precision)
+    transport = "nccl" if world > 1 else "local"
+    steps = max(1, min(args.steps, 2))
+
+    def once():
+        return P.run_3way(e2e_prob, grid, transport=transport, keep_values=False).checksum.hex
+
+    once()  # warm-up (allocations)
+    times = []
+    for _ in range(steps):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        cks = once()
+        times.append(time.perf_counter() - t0)
+    el = statistics.median(times)
+    if world > 1:
+        t = torch.tensor([el], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el = float(t.item())
+    isz = 8 if precision == "double" else 4
+    return {"value": total_cmp / el, "unit": "comparisons/s",
+            "h2d_bytes_per_step": prob.n_f * prob.n_v * isz,
+            "d2h_bytes_per_step": 32 * world,
+            "seconds_per_step": el, "checksum": cks,
+            "values_path": "reduced on the device to the 128-bit checksum (values exceed host "
+                           "memory)",
+            "api": f"paper_1705_08210_b200.run_3way(Problem(3, n_f, n_v, pinned slab source), "
+                   f"grid, transport='{transport}', keep_values=False)"}
 
 
 class SlabSource:
