@@ -147,6 +147,16 @@ int psim_czek2_tasks(int dtype, const psim_block2_t* tasks, int ntasks, void* st
  * bits zero); flags[0] += #entries outside {0, 1} (DataError). */
 int psim_pack_bits(int dtype, const void* V, int64_t n_fp, int64_t n_vp, int64_t ld,
                    uint32_t* words, int64_t ldw, unsigned long long* flags, void* stream);
+/* mgemm_bitpacked (mingemm.py:294-312): raw counts M[i + j * ldm] = popcount
+ * of W_i & V_j over n_rows bits, int64, column-major (ldm >= m). W / V as for
+ * psim_pack_bits (16-byte aligned, ld in words, a multiple of 4). */
+int psim_mgemm_bits(const uint32_t* W, int64_t ldw, const uint32_t* V, int64_t ldv,
+                    int64_t n_rows, int64_t m, int64_t n, int64_t* M, int64_t ldm, void* stream);
+/* xj_columns (mingemm.py:225-234): out[k * ldo + q] = min(vj[q], V[k * ld + q])
+ * for the n_vp columns of V (the 3-way pivot columns; fused into the 3-way
+ * mainloop elsewhere). */
+int psim_min_columns(int dtype, const void* V, int64_t n_fp, int64_t n_vp, int64_t ld,
+                     const void* vj, void* out, int64_t ldo, void* stream);
 /* Sorenson 2-way task on packed operands (W, V = word arrays, ldw / ldv in
  * words, n_f in fields): counts popcount(a & b) (mgemm_bitpacked,
  * mingemm.py:294-312), converted to the run dtype, then the 2-way value,

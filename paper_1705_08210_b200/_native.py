@@ -88,6 +88,9 @@ SIGNATURES = {
     "psim_stream_stats": (C.c_int, [C.POINTER(C.c_uint64), C.c_int]),
     "psim_quantize_bytes": (C.c_int, [C.c_int, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "psim_box3_plan": (C.c_int, [C.c_int, C.POINTER(Box3), C.POINTER(c_i64), C.POINTER(c_i64)]),
+    "psim_mgemm_bits": (C.c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64,
+                                  c_vp]),
+    "psim_min_columns": (C.c_int, [C.c_int, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp]),
     "psim_box3_tile": (C.c_int, [C.c_int, C.POINTER(Box3), C.c_int, c_i64, C.POINTER(c_i64),
                                  C.POINTER(c_i64)]),
     "psim_czek3_box": (C.c_int, [C.c_int, C.POINTER(Box3), c_vp]),

@@ -189,6 +189,32 @@ int psim_pack_bits(int dtype, const void* V, int64_t n_fp, int64_t n_vp, int64_t
                      "psim_pack_bits");
 }
 
+int psim_mgemm_bits(const uint32_t* W, int64_t ldw, const uint32_t* V, int64_t ldv,
+                    int64_t n_rows, int64_t m, int64_t n, int64_t* M, int64_t ldm, void* stream) {
+  if (n_rows < 0 || m < 0 || n < 0) return fail(PSIM_ECONFIG, "negative extent");
+  if (m == 0 || n == 0) return PSIM_OK;
+  if (!W || !V || !M) return fail(PSIM_ECONFIG, "NULL operand");
+  const int64_t nw = (n_rows + 31) / 32;
+  if (ldw < nw || ldv < nw || ldw % 4 || ldv % 4 || reinterpret_cast<uintptr_t>(W) % 16 ||
+      reinterpret_cast<uintptr_t>(V) % 16)
+    return fail(PSIM_ECONFIG, "packed operands need 16-byte alignment and ld >= ceil(n_rows/32)");
+  if (ldm < m) return fail(PSIM_ECONFIG, "ldm=%lld < m=%lld", (long long)ldm, (long long)m);
+  return cuda_status(psim::mgemm_bits(W, ldw, V, ldv, n_rows, m, n,
+                                      reinterpret_cast<long long*>(M), ldm, S(stream)),
+                     "psim_mgemm_bits");
+}
+
+int psim_min_columns(int dtype, const void* V, int64_t n_fp, int64_t n_vp, int64_t ld,
+                     const void* vj, void* out, int64_t ldo, void* stream) {
+  if (int r = check_dtype(dtype)) return r;
+  if (n_fp < 0 || n_vp < 0) return fail(PSIM_ECONFIG, "negative extent");
+  if (n_fp == 0 || n_vp == 0) return PSIM_OK;
+  if (!V || !vj || !out || ld < n_fp || ldo < n_fp)
+    return fail(PSIM_ECONFIG, "bad operand / leading dimension");
+  return cuda_status(psim::min_columns(dtype, V, n_fp, n_vp, ld, vj, out, ldo, S(stream)),
+                     "psim_min_columns");
+}
+
 int psim_sorenson2_block(int dtype, const psim_block2_t* t, void* stream) {
   if (int r = check_dtype(dtype)) return r;
   if (!t || !t->W || !t->V || !t->s_row || !t->s_col || !t->acc)

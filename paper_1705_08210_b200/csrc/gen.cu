@@ -167,6 +167,35 @@ cudaError_t fold_add(int dtype, void* dst, const void* src, int64_t count, cudaS
   return cudaGetLastError();
 }
 
+// xj_columns (mingemm.py:225-234): out[:, k] = np.minimum(v_j, V[:, k]),
+// numpy's rule (x < y || x is NaN) ? x : y, so signed zeros and NaNs match.
+template <typename T>
+__global__ void k_min_columns(const T* __restrict__ V, int64_t n_fp, int64_t n_vp, int64_t ld,
+                              const T* __restrict__ vj, T* __restrict__ out, int64_t ldo) {
+  const int64_t total = n_fp * n_vp;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = e / n_fp, q = e - k * n_fp;
+    const T x = vj[q], y = V[k * ld + q];
+    out[k * ldo + q] = (x < y || x != x) ? x : y;
+  }
+}
+
+cudaError_t min_columns(int dtype, const void* V, int64_t n_fp, int64_t n_vp, int64_t ld,
+                        const void* vj, void* out, int64_t ldo, cudaStream_t st) {
+  if (n_fp <= 0 || n_vp <= 0) return cudaSuccess;
+  const unsigned g = grid_for(n_fp * n_vp, 256);
+  if (dtype == kF64)
+    k_min_columns<double><<<g, 256, 0, st>>>(static_cast<const double*>(V), n_fp, n_vp, ld,
+                                             static_cast<const double*>(vj),
+                                             static_cast<double*>(out), ldo);
+  else
+    k_min_columns<float><<<g, 256, 0, st>>>(static_cast<const float*>(V), n_fp, n_vp, ld,
+                                            static_cast<const float*>(vj),
+                                            static_cast<float*>(out), ldo);
+  return cudaGetLastError();
+}
+
 // Byte output mode (io.py:122-136): floor(clamp(v, 0, 1) * 255 + 0.5) in
 // double, the multiply and add rounded separately (no FMA contraction) so the
 // byte equals numpy's. Eight values per thread: one 8-byte store.

@@ -45,6 +45,11 @@ constexpr int64_t kStreamMaxFlags = 65536;  // data + sum flags of a streamed ru
 cudaError_t pack_bits(int dtype, const void* V, int64_t n_fp, int64_t n_vp, int64_t ld,
                       uint32_t* words, int64_t ldw, unsigned long long* flags, cudaStream_t st);
 cudaError_t sorenson2_block(int dtype, const psim_block2_t& t, cudaStream_t st);
+cudaError_t mgemm_bits(const uint32_t* W, int64_t ldw, const uint32_t* V, int64_t ldv,
+                       int64_t n_rows, int64_t m, int64_t n, long long* M, int64_t ldm,
+                       cudaStream_t st);
+cudaError_t min_columns(int dtype, const void* V, int64_t n_fp, int64_t n_vp, int64_t ld,
+                        const void* vj, void* out, int64_t ldo, cudaStream_t st);
 // Several 2-way tasks (same n_f, n_v, dtype) in one grid (<= 16 per launch).
 cudaError_t czek2_tasks(int dtype, const Czek2Block* tasks, int ntasks, cudaStream_t st);
 cudaError_t mgemm(int dtype, const void* W, int64_t ldw, const void* V, int64_t ldv, int64_t n_f,

@@ -185,6 +185,50 @@ static cudaError_t sorenson_t(const psim_block2_t& t, cudaStream_t st) {
   return e != cudaSuccess ? e : e2;
 }
 
+// Raw counts (mgemm_bitpacked itself, mingemm.py:294-312): M[i + j*ldm] =
+// sum over words of popc(W_i & V_j), int64, column-major; the kernel
+// plug-point form (no epilogue), row-major tile order.
+__global__ void __launch_bounds__(kNT, CfgBits::MINB)
+    k_mgemm_bits(const uint32_t* __restrict__ W, int64_t ldw, const uint32_t* __restrict__ V,
+                 int64_t ldv, int64_t n_words, int64_t m, int64_t n, int64_t tiles_n,
+                 long long* __restrict__ M, int64_t ldm) {
+  using C = CfgBits;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* smem = reinterpret_cast<uint32_t*>(smem_raw);
+  const int64_t bi = blockIdx.x / tiles_n, bj = blockIdx.x - bi * tiles_n;
+  const int64_t row0 = bi * C::BM, col0 = bj * C::BN;
+  const int rows = (int)min64(C::BM, m - row0), cols = (int)min64(C::BN, n - col0);
+  uint32_t acc[C::TM][C::TN];
+  minplus_tile<C, false>(W + row0 * ldw, ldw, rows, V + col0 * ldv, ldv, cols, nullptr, n_words,
+                         acc, smem);
+  const int ty = thread_ty(), tx = thread_tx();
+#pragma unroll
+  for (int mi = 0; mi < C::TM; ++mi) {
+    const int li = ty + 16 * mi;
+#pragma unroll
+    for (int nj = 0; nj < C::TN; ++nj) {
+      const int lj = tx + 16 * nj;
+      if (li < rows && lj < cols) M[(row0 + li) + (col0 + lj) * ldm] = (long long)acc[mi][nj];
+    }
+  }
+}
+
+cudaError_t mgemm_bits(const uint32_t* W, int64_t ldw, const uint32_t* V, int64_t ldv,
+                       int64_t n_rows, int64_t m, int64_t n, long long* M, int64_t ldm,
+                       cudaStream_t st) {
+  using C = CfgBits;
+  if (m <= 0 || n <= 0) return cudaSuccess;
+  const int64_t tiles_n = (n + C::BN - 1) / C::BN;
+  const int64_t blocks = ((m + C::BM - 1) / C::BM) * tiles_n;
+  if (blocks > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  cudaError_t e = cudaFuncSetAttribute(k_mgemm_bits, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       C::SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  k_mgemm_bits<<<(unsigned)blocks, kNT, C::SMEM_BYTES, st>>>(W, ldw, V, ldv, (n_rows + 31) / 32,
+                                                             m, n, tiles_n, M, ldm);
+  return cudaGetLastError();
+}
+
 cudaError_t sorenson2_block(int dtype, const psim_block2_t& t, cudaStream_t st) {
   return dtype == kF64 ? sorenson_t<double>(t, st) : sorenson_t<float>(t, st);
 }

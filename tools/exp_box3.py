@@ -44,6 +44,10 @@ def main():
         "volume 2000^3 (ragged edges)": Box((0, 0, 0), 0, 2000, 2048, 4048, 4096, 6096),
         "diag pivots [2000,2600) full k": Box((0, 0, 0), 0, n, 2000, 2600, 0, n),
         "diag pivots [0,6144) k in [0,1024)": Box((0, 0, 0), 0, n, 0, n, 0, 1024),
+        "face I<J=K 3000 rows (FLAT_COLS)": Box((0, 0, 0), 0, 3000, 3000, 6000, 3000, 6000),
+        "face I=J<K 3000 cols (FLAT_ROWS)": Box((0, 0, 0), 0, 3000, 0, 3000, 3000, 6000),
+        "face small 512 x 1024 (FLAT_COLS)": Box((0, 0, 0), 0, 512, 2048, 3072, 2048, 3072),
+        "diag 3000 (PAIR)": Box((0, 0, 0), 0, 3000, 0, 3000, 0, 3000),
     }
     for name, box in cases.items():
         if only and only not in name:
