@@ -169,6 +169,32 @@ def fold_over_field(local_parts: torch.Tensor, code: int, group, n_pf: int) -> t
     return total
 
 
+def exchange_ops(own, own_sums, recv, recv_sums, send_rank: int, recv_rank: int) -> list:
+    """One circulant step (metrics2.py:140-147, RankContext.send/receive
+    engine.py:177-184): ship the own block and its sums to ``send_rank``,
+    receive the peer block and sums from ``recv_rank`` -- one grouped
+    send/recv (batch_isend_irecv)."""
+    return [
+        dist.P2POp(dist.isend, own, send_rank),
+        dist.P2POp(dist.isend, own_sums, send_rank),
+        dist.P2POp(dist.irecv, recv, recv_rank),
+        dist.P2POp(dist.irecv, recv_sums, recv_rank),
+    ]
+
+
+def allgather_ops(me: int, n_pv: int, blocks: dict, sums: dict, peer) -> list:
+    """The 3-way block circulation (face_j / vol_k / vol_j exchanges,
+    metrics3.py:93-109) as one circulant all-gather: slab ``me`` sends its
+    block and sums to me - d and receives slab me + d's, d = 1 .. n_pv - 1
+    (blocks / sums: slab -> buffer; peer: slab -> rank)."""
+    ops = []
+    for d in range(1, n_pv):
+        ops.extend(exchange_ops(blocks[me], sums[me], blocks[(me + d) % n_pv],
+                                sums[(me + d) % n_pv], peer((me - d) % n_pv),
+                                peer((me + d) % n_pv)))
+    return ops
+
+
 class Runner2:
     """One rank's 2-way pipeline over NCCL (also the multi-GPU bench harness)."""
 
@@ -228,13 +254,9 @@ class Runner2:
         return s
 
     def _post_exchange(self, ev: Exchange, slot: int, s_own: torch.Tensor):
-        ops = [
-            dist.P2POp(dist.isend, self.own.data, self.peer(ev.send_to)),
-            dist.P2POp(dist.isend, s_own, self.peer(ev.send_to)),
-            dist.P2POp(dist.irecv, self.remote[slot].data, self.peer(ev.recv_from)),
-            dist.P2POp(dist.irecv, self.remote_sums[slot], self.peer(ev.recv_from)),
-        ]
-        return dist.batch_isend_irecv(ops)
+        return dist.batch_isend_irecv(exchange_ops(
+            self.own.data, s_own, self.remote[slot].data, self.remote_sums[slot],
+            self.peer(ev.send_to), self.peer(ev.recv_from)))
 
     def _step_fused(self, s_own, timed: bool) -> list:
         p = self.problem

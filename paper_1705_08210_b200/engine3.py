@@ -367,14 +367,10 @@ class Runner3Dist:
         self.tables.cache.clear()
         works = []
         if g.n_pv > 1:
-            ops = []
-            for d in range(1, g.n_pv):
-                ops.append(dist.P2POp(dist.isend, own.data, self.peer(me - d)))
-                ops.append(dist.P2POp(dist.isend, self.sums[me], self.peer(me - d)))
-                src = (me + d) % g.n_pv
-                ops.append(dist.P2POp(dist.irecv, self.blocks[src].data, self.peer(src)))
-                ops.append(dist.P2POp(dist.irecv, self.sums[src], self.peer(src)))
-            works = dist.batch_isend_irecv(ops)
+            from .dist import allgather_ops
+
+            data = {slab: b.data for slab, b in self.blocks.items()}
+            works = dist.batch_isend_irecv(allgather_ops(me, g.n_pv, data, self.sums, self.peer))
         events: list = []
         self._run(self.edge_boxes, timed, events)
         for w in works:

@@ -125,3 +125,73 @@ def test_distributed_output_writer_gloo(tmp_path):
     from test_output import check_directory
 
     check_directory(tmp_path, case)
+
+
+def _exchange_worker(rank, world, port, q):
+    """2-way circulant steps (every Exchange of plan_2way, posted all at once as
+    the fused NCCL runner does, then one at a time) and the 3-way all-gather,
+    through the runners' own op builders, on CPU tensors."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1705_08210_b200 import DecompGrid
+        from paper_1705_08210_b200 import dist as PD
+        from paper_1705_08210_b200.domain import coords_of_rank, rank_of_coords
+        from paper_1705_08210_b200.plan import Exchange, plan_2way
+
+        grid = DecompGrid(n_pv=world)
+        c = coords_of_rank(rank, grid)
+        me = c.p_v
+        peer = lambda slab: rank_of_coords(type(c)(c.p_f, slab % world, c.p_r), grid)  # noqa: E731
+        own = torch.full((3, 4), float(me))
+        s_own = torch.full((3,), 10.0 + me)
+        exs = [e for e in plan_2way(grid, c, 12, "split") if isinstance(e, Exchange)]
+        ok = []
+        for fused in (True, False):
+            bufs = [(torch.empty(3, 4), torch.empty(3)) for _ in exs]
+            works = []
+            for e, (b, s) in zip(exs, bufs):
+                w = dist.batch_isend_irecv(PD.exchange_ops(own, s_own, b, s, peer(e.send_to),
+                                                           peer(e.recv_from)))
+                if fused:
+                    works.extend(w)
+                else:
+                    for x in w:
+                        x.wait()
+            for x in works:
+                x.wait()
+            for e, (b, s) in zip(exs, bufs):
+                src = (me + e.step) % world
+                ok.append(bool((b == src).all()) and bool((s == 10.0 + src).all()))
+        blocks = {sl: (own if sl == me else torch.empty(3, 4)) for sl in range(world)}
+        sums = {sl: (s_own if sl == me else torch.empty(3)) for sl in range(world)}
+        for x in dist.batch_isend_irecv(PD.allgather_ops(me, world, blocks, sums, peer)):
+            x.wait()
+        ok.append(all(bool((blocks[sl] == sl).all()) and bool((sums[sl] == 10.0 + sl).all())
+                      for sl in range(world)))
+        q.put((rank, len(exs), ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [8])
+def test_circulant_exchanges_and_allgather_gloo(world):
+    """n_pv = 8 (the size no GPU run here covers): every block arrives from the
+    slab the plan names, in fused and stepwise posting, and the 3-way
+    all-gather delivers every slab to every rank."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_exchange_worker, args=(r, world, port, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    results = dict((r, (n, ok)) for r, n, ok in (q.get(timeout=10) for _ in range(world)))
+    for r in range(world):
+        n, ok = results[r]
+        assert n == world // 2  # steps 1 .. n_pv/2 (the last one split, schedule.py:128-136)
+        assert all(ok), (r, ok)
