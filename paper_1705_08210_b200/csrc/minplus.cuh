@@ -288,6 +288,12 @@ __device__ __forceinline__ void minplus_tile(const typename C::T* __restrict__ W
 
   const int KT = (int)((n_f + C::BK - 1) / C::BK);
   constexpr int XS = (C::BM + C::BN) * C::PITCH;  // pivot slot offset inside a stage
+  // PIVOT with >= 4 stages: the pivot min of stage kt+1 is applied in
+  // iteration kt, right after the one barrier that also publishes stage kt,
+  // so a 3-way tile needs no second barrier per stage (one stage less of
+  // prefetch depth). Each thread rewrites exactly the chunks its own
+  // cp.asyncs brought in; the barrier publishes the pivot chunk.
+  constexpr bool AHEAD = PIVOT && S >= 4;
 #pragma unroll
   for (int s = 0; s < S - 1; ++s) {
     if (s < KT) {
@@ -296,11 +302,25 @@ __device__ __forceinline__ void minplus_tile(const typename C::T* __restrict__ W
     }
     cp_async_commit();
   }
-  for (int kt = 0; kt < KT; ++kt) {
+  if (AHEAD && KT > 0) {
     cp_async_wait<S - 2>();
     __syncthreads();
+    stage_pivot_min<C>(smem, smem + XS);
+  }
+  for (int kt = 0; kt < KT; ++kt) {
+    if constexpr (AHEAD) {
+      cp_async_wait<(AHEAD ? S - 3 : 0)>();
+    } else {
+      cp_async_wait<S - 2>();
+    }
+    __syncthreads();
     T* st = smem + (kt % S) * C::STAGE_ELEMS;
-    if (PIVOT) {
+    if constexpr (AHEAD) {
+      if (kt + 1 < KT) {
+        T* nx = smem + ((kt + 1) % S) * C::STAGE_ELEMS;
+        stage_pivot_min<C>(nx, nx + XS);
+      }
+    } else if (PIVOT) {
       // (measured: transforming own chunks before the barrier with the pivot
       // staged one group early was 3% slower than this extra barrier)
       stage_pivot_min<C>(st, st + XS);
