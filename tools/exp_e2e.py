@@ -54,6 +54,7 @@ def main():
             P.run_2way(prob, P.DecompGrid(), host_values=host_values)  # warm-up
             for _ in range(reps):
                 torch.cuda.synchronize()
+                m0 = torch.cuda.memory_stats()
                 with ClockSampler(0, 0.02) as clk:
                     t0 = time.perf_counter()
                     res = P.run_2way(prob, P.DecompGrid(), host_values=host_values)
@@ -69,7 +70,14 @@ def main():
                                   "sum_wait_sm_ms": st[1] / 1e6, "sum_waits": st[2],
                                   "max_wait_ms": st[3] / 1e6, "call_s": round(el_dev, 4),
                                   "mhz_min": mhz[0], "mhz_med": mhz[len(mhz) // 2],
-                                  "reasons": sorted({r for _, r in clk.samples})}), flush=True)
+                                  "reasons": sorted({r for _, r in clk.samples}),
+                                  "dev_segments_new": torch.cuda.memory_stats().get(
+                                      "segment.all.allocated", 0) - m0.get("segment.all.allocated", 0),
+                                  "alloc_retries": torch.cuda.memory_stats().get(
+                                      "num_alloc_retries", 0) - m0.get("num_alloc_retries", 0),
+                                  "host_segments": torch.cuda.host_memory_stats().get(
+                                      "segment.allocated", torch.cuda.host_memory_stats().get(
+                                          "num_host_alloc", -1))}), flush=True)
                 del res
     # pinned allocation reuse
     for _ in range(3):
