@@ -118,14 +118,30 @@ def block_from_host(host: torch.Tensor, n_fp: int, v0: int, precision: str, devi
     return Block(data, n_fp, n_vp, data.shape[1], v0, precision)
 
 
-def check_values(data, n_fp, n_vp, ld, code) -> None:
+def check_values_async(data, n_fp, n_vp, ld, code) -> torch.Tensor:
+    """Enqueue the device validation; returns the flags for raise_on_flags."""
     flags = torch.zeros(2, dtype=torch.int64, device=data.device)
     N.call("psim_check_block", code, ptr(data), n_fp, n_vp, ld, ptr(flags), stream_ptr())
+    return flags
+
+
+def raise_on_flags(flags: torch.Tensor) -> None:
+    import os
+
+    if os.environ.get("PSIM_POLL") == "1":  # experiment: busy-poll instead of a blocking read
+        ev = torch.cuda.Event()
+        ev.record()
+        while not ev.query():
+            pass
     bad, neg = (int(x) for x in flags.cpu())
     if bad:
         raise DataError("non-finite element in vector block")
     if neg:
         raise DataError("negative element in vector block")
+
+
+def check_values(data, n_fp, n_vp, ld, code) -> None:
+    raise_on_flags(check_values_async(data, n_fp, n_vp, ld, code))
 
 
 def column_sums(block: Block) -> torch.Tensor:

@@ -160,6 +160,23 @@ def pinned_host_block(problem, grid):
     return host if host.is_pinned() else None
 
 
+# PSIM_TRACE=1: run_streamed records CUDA events (and host clocks) at its
+# phase boundaries into LAST_TRACE [(name, event, perf_counter)]
+# (diagnostics for tools/exp_e2e.py)
+LAST_TRACE: list = []
+
+
+def _mark(name: str) -> None:
+    import os
+
+    if os.environ.get("PSIM_TRACE") == "1":
+        import time
+
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        LAST_TRACE.append((name, ev, time.perf_counter()))
+
+
 def run_streamed(problem, host: torch.Tensor, keep_values: bool, sink) -> Outcome:
     """Single-slab run whose input is still in pinned host memory: the copy
     engine uploads the block in chunks (last vectors first) while the fused
@@ -175,7 +192,9 @@ def run_streamed(problem, host: torch.Tensor, keep_values: bool, sink) -> Outcom
     tdt = D.torch_dtype(problem.precision)
     copy = _COPY_STREAM.setdefault(dev.index, torch.cuda.Stream(device=dev))
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    LAST_TRACE.clear()
     start.record()
+    _mark("start")
     data = D.alloc_block(n_f, n, problem.precision, dev)
     ld = data.shape[1]
     chunk = max(256, -(-n // 64))
@@ -191,10 +210,16 @@ def run_streamed(problem, host: torch.Tensor, keep_values: bool, sink) -> Outcom
     t = N.Block2(W=data.data_ptr(), ldw=ld, V=data.data_ptr(), ldv=ld, n_f=n_f, m=n, n=n,
                  diagonal=1, g_row=0, g_col=0, n_v=n, vals=D.ptr(vals), acc=acc.data_ptr(),
                  s_row=sums.data_ptr())
+    _mark("buffers")
     N.call("psim_czek2_streamed", code, C.byref(t), host.data_ptr(), n_f, chunk,
            ready.data_ptr(), D.stream_ptr(), copy.cuda_stream)
+    _mark("kernel")
     torch.cuda.current_stream().wait_stream(copy)
-    D.check_values(data, n_f, n, ld, code)  # raises DataError like VectorBlock (core.py:239-242)
+    _mark("copies")
+    flags = D.check_values_async(data, n_f, n, ld, code)
+    _mark("check")
+    D.raise_on_flags(flags)  # DataError like VectorBlock (core.py:239-242)
+    _mark("checked")
     end.record()
     end.synchronize()
     lo, hi, deg = D.acc_words(acc)

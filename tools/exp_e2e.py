@@ -48,6 +48,9 @@ def main():
 
     reps = int(os.environ.get("REPS", "4"))
     modes = os.environ.get("MODES", "1,0").split(",")
+    os.environ["PSIM_TRACE"] = "1"
+    from paper_1705_08210_b200 import engine2
+
     for streamed in modes:
         for host_values in (True, False):
             os.environ["PSIM_STREAMED"] = streamed
@@ -73,6 +76,11 @@ def main():
                                   "reasons": sorted({r for _, r in clk.samples}),
                                   "dev_segments_new": torch.cuda.memory_stats().get(
                                       "segment.all.allocated", 0) - m0.get("segment.all.allocated", 0),
+                                  "trace_ms": {b[0]: round(a[1].elapsed_time(b[1]), 3) for a, b in
+                                               zip(engine2.LAST_TRACE, engine2.LAST_TRACE[1:])},
+                                  "host_trace_ms": {b[0]: round((b[2] - a[2]) * 1e3, 3) for a, b in
+                                                    zip(engine2.LAST_TRACE,
+                                                        engine2.LAST_TRACE[1:])},
                                   "alloc_retries": torch.cuda.memory_stats().get(
                                       "num_alloc_retries", 0) - m0.get("num_alloc_retries", 0),
                                   "host_segments": torch.cuda.host_memory_stats().get(
