@@ -318,8 +318,7 @@ __host__ __device__ inline Tile3 box3_decode(const psim_box3_t& b, const int64_t
     return d;
   }
   l -= nC;
-  const int64_t nD = g.w + h.w > 0 ? g.R : 0;
-  {  // ragged leading columns of both pivots in one tile (l < nD)
+  {  // ragged leading columns of both pivots in one tile (l < R when g.w + h.w > 0)
     d.side = 1;
     d.p1 = q;
     d.row0 = b.i0 + l * BM;

@@ -34,6 +34,12 @@
 namespace psim {
 
 constexpr int kNT = 256;  // threads per CTA (16 x 16)
+
+// Unroll factor of the per-stage micro-step loop: measured (exp_minplus,
+// profiles/r01_unroll_sweep.jsonl) FP64 best rolled (1: the 8.5 KB body stays
+// in the instruction cache; +0.9% vs full), FP32 best at 4 (+0.7%).
+// -DPSIM_KK_UNROLL=u overrides it for experiments.
+
 constexpr int kPitchBytes = 144;
 
 // Tile configuration: TM x TN per thread, STAGES-deep cp.async pipeline,
@@ -51,6 +57,12 @@ struct Cfg {
   static constexpr int VEC = 16 / (int)sizeof(T);    // q per LDS.128
   static constexpr int PITCH = kPitchBytes / (int)sizeof(T);
   static constexpr int STAGE_ELEMS = (BM + BN) * PITCH + 2 * BK;  // A, B, 2 pivot chunks
+#ifdef PSIM_KK_UNROLL
+  static constexpr int KKU = PSIM_KK_UNROLL;
+#else
+  static constexpr int KKU = std::is_same<T_, double>::value ? 1
+                             : std::is_same<T_, float>::value ? 4 : BK / VEC;
+#endif
   static constexpr int SMEM_BYTES = STAGES * STAGE_ELEMS * (int)sizeof(T);
   static_assert((BM * 8) % kNT == 0 && (BN * 8) % kNT == 0, "tile / thread mismatch");
   static_assert(sizeof(T) == 8 || TN % 2 == 0, "FP32 pairs columns for FADD2");
@@ -121,7 +133,7 @@ __device__ __forceinline__ void micro_step(float (&acc)[C::TM][C::TN], const flo
 #pragma unroll
   for (int m = 0; m < C::TM; ++m)
     a[m] = *reinterpret_cast<const float4*>(As + (ty + 16 * m) * P + kk);
-  if (C::VAR % 2 == 1) {  // scalar adds
+  if constexpr (C::VAR % 2 == 1) {  // scalar adds
 #pragma unroll
     for (int n = 0; n < C::TN; ++n) {
       const float4 b = *reinterpret_cast<const float4*>(Bs + (tx + 16 * n) * P + kk);
@@ -134,8 +146,7 @@ __device__ __forceinline__ void micro_step(float (&acc)[C::TM][C::TN], const flo
 #pragma unroll
       for (int m = 0; m < C::TM; ++m) acc[m][n] = __fadd_rn(acc[m][n], fmin_v<C::VAR>(a[m].w, b.w));
     }
-    return;
-  }
+  } else {
 #pragma unroll
   for (int n = 0; n < C::TN; n += 2) {
     const float4 b0 = *reinterpret_cast<const float4*>(Bs + (tx + 16 * n) * P + kk);
@@ -152,6 +163,7 @@ __device__ __forceinline__ void micro_step(float (&acc)[C::TM][C::TN], const flo
 #pragma unroll
     for (int m = 0; m < C::TM; ++m)
       fadd2(acc[m][n], acc[m][n + 1], fmin_v<C::VAR>(a[m].w, b0.w), fmin_v<C::VAR>(a[m].w, b1.w));
+  }
   }
 }
 
@@ -351,7 +363,9 @@ __device__ __forceinline__ void minplus_tile(const typename C::T* __restrict__ W
     }
     const T* As = st;
     const T* Bs = st + C::BM * C::PITCH;
-#pragma unroll
+    // (the 3-way pivot loop keeps the full unroll: rolled it measured 2% slower)
+    constexpr int U = PIVOT ? C::BK / C::VEC : C::KKU;
+#pragma unroll U
     for (int kk = 0; kk < C::BK; kk += C::VEC) micro_step<C>(acc, As, Bs, ty, tx, kk);
   }
   cp_async_wait<0>();

@@ -128,11 +128,15 @@ def check_values_async(data, n_fp, n_vp, ld, code) -> torch.Tensor:
 def raise_on_flags(flags: torch.Tensor) -> None:
     import os
 
-    if os.environ.get("PSIM_POLL") == "1":  # experiment: busy-poll instead of a blocking read
+    poll = os.environ.get("PSIM_POLL")
+    if poll in ("1", "2"):  # experiment: poll (1 busy, 2 with 0.5 ms sleeps) before the read
+        import time
+
         ev = torch.cuda.Event()
         ev.record()
         while not ev.query():
-            pass
+            if poll == "2":
+                time.sleep(0.0005)
     bad, neg = (int(x) for x in flags.cpu())
     if bad:
         raise DataError("non-finite element in vector block")

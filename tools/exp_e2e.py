@@ -52,13 +52,20 @@ def main():
     from paper_1705_08210_b200 import engine2
 
     for streamed in modes:
-        for host_values in (True, False):
+        for host_values in ((True, False) if os.environ.get("HV") is None
+                            else (os.environ["HV"] == "1",)):
             os.environ["PSIM_STREAMED"] = streamed
             P.run_2way(prob, P.DecompGrid(), host_values=host_values)  # warm-up
             for _ in range(reps):
                 torch.cuda.synchronize()
                 m0 = torch.cuda.memory_stats()
-                with ClockSampler(0, 0.02) as clk:
+                if os.environ.get("NOGC") == "1":
+                    import gc
+
+                    gc.collect()
+                    gc.disable()
+                with (ClockSampler(0, 0.02) if os.environ.get("NOCLK") != "1"
+                      else ClockSampler(0, 3600.0)) as clk:
                     t0 = time.perf_counter()
                     res = P.run_2way(prob, P.DecompGrid(), host_values=host_values)
                     el_dev = time.perf_counter() - t0

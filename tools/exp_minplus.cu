@@ -91,8 +91,10 @@ void run(const char* name, int64_t n, int64_t n_f) {
 int main(int argc, char** argv) {
   int64_t n = argc > 1 ? atoll(argv[1]) : 8192;
   int64_t nf = argc > 2 ? atoll(argv[2]) : 20000;
-  run<Cfg<double, 8, 8, 4, 1, 0>>("f64_8x8_s4_v0", n, nf);
-  run<Cfg<double, 16, 4, 3, 1, 0>>("f64_16x4_s3_v0", n, nf);
-  run<Cfg<double, 4, 16, 3, 1, 0>>("f64_4x16_s3_v0", n, nf);
+  char name[64];
+  snprintf(name, sizeof name, "f64_8x8_s4_u%d", PSIM_KK_UNROLL);
+  run<Cfg<double, 8, 8, 4, 1, 0>>(name, n, nf);
+  snprintf(name, sizeof name, "f32_8x4_s3_b2_v1_u%d", PSIM_KK_UNROLL);
+  run<Cfg<float, 8, 4, 3, 2, 1>>(name, n, (nf * 5) / 2);
   return 0;
 }
