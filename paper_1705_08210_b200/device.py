@@ -125,19 +125,38 @@ def check_values_async(data, n_fp, n_vp, ld, code) -> torch.Tensor:
     return flags
 
 
+def spin_event(ev) -> None:
+    """Wait for a recorded CUDA event by spinning on cudaEventQuery.
+
+    Measured on the B200 boxes (tools/exp_sync.cu, profiles/
+    r01_host_sync_latency.jsonl): after a multi-second kernel a blocking wait
+    (cudaEventSynchronize, with the default, spin or blocking-sync schedule)
+    returned 1-650 ms late; a tight query loop returned within 0.1 ms. Every
+    host wait of the run paths after their main kernels goes through here."""
+    while not ev.query():
+        pass
+
+
+def spin_wait() -> None:
+    """spin_event on an event recorded now on the current stream."""
+    ev = torch.cuda.Event()
+    ev.record()
+    spin_event(ev)
+
+
+def to_host(t: torch.Tensor) -> np.ndarray:
+    """A small device tensor as numpy, through a pinned buffer and spin_wait
+    (no blocking copy)."""
+    if not t.is_cuda:
+        return t.numpy()
+    host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    host.copy_(t, non_blocking=True)
+    spin_wait()
+    return host.numpy()
+
+
 def raise_on_flags(flags: torch.Tensor) -> None:
-    import os
-
-    poll = os.environ.get("PSIM_POLL")
-    if poll in ("1", "2"):  # experiment: poll (1 busy, 2 with 0.5 ms sleeps) before the read
-        import time
-
-        ev = torch.cuda.Event()
-        ev.record()
-        while not ev.query():
-            if poll == "2":
-                time.sleep(0.0005)
-    bad, neg = (int(x) for x in flags.cpu())
+    bad, neg = (int(x) for x in to_host(flags))
     if bad:
         raise DataError("non-finite element in vector block")
     if neg:
@@ -166,7 +185,7 @@ def new_acc(device) -> torch.Tensor:
 
 
 def acc_words(acc: torch.Tensor) -> tuple[int, int, int]:
-    lo, hi, deg = (int(x) & ((1 << 64) - 1) for x in acc.cpu().tolist())
+    lo, hi, deg = (int(x) & ((1 << 64) - 1) for x in to_host(acc).tolist())
     return lo, hi, deg
 
 

@@ -102,13 +102,13 @@ def piece_count(pc) -> int:
 
 def gather_totals(acc: torch.Tensor, count: int, world: int, dev) -> tuple[int, int, int, int]:
     """All-gather every rank's (checksum lo, hi, degenerate, count); sum mod 2^128."""
-    mine = torch.tensor([*acc.tolist(), count], dtype=torch.int64, device=dev)
+    mine = torch.tensor([*D.to_host(acc).tolist(), count], dtype=torch.int64, device=dev)
     allv = torch.empty(world * 4, dtype=torch.int64, device=dev)
     dist.all_gather_into_tensor(allv, mine)
     allv = allv.view(world, 4)
     M64 = (1 << 64) - 1
     total = deg = cnt = 0
-    for lo, hi, d, c in allv.cpu().tolist():
+    for lo, hi, d, c in D.to_host(allv).tolist():
         total += ((hi & M64) << 64) | (lo & M64)
         deg += d
         cnt += c
@@ -392,7 +392,7 @@ class Runner2:
         out = torch.empty(self.world * self.n_vp, dtype=self.s_own.dtype, device=self.dev)
         dist.all_gather_into_tensor(out, self.s_own.contiguous())
         out = out.view(self.world, self.n_vp)
-        host = out.cpu().numpy()
+        host = D.to_host(out)
         sums = np.empty(self.problem.n_v, dtype=host.dtype)
         for r in range(self.world):
             c = coords_of_rank(r, self.grid)
@@ -414,7 +414,7 @@ def run_2way_nccl(problem, grid, balance: str = "split", keep_values: bool = Tru
     r.setup()
     r.step()
     end.record()
-    end.synchronize()
+    D.spin_event(end)
     if r.sink is not None:
         r.sink.finish()
     el = torch.tensor([start.elapsed_time(end) * 1e-3], dtype=torch.float64, device=r.dev)
@@ -422,7 +422,7 @@ def run_2way_nccl(problem, grid, balance: str = "split", keep_values: bool = Tru
     lo, hi, deg, cnt = r.totals()
     sums = r.global_sums()
     pieces = r.pieces
-    return Outcome(pieces, lo, hi, deg, cnt, sums, float(el.item()),
+    return Outcome(pieces, lo, hi, deg, cnt, sums, float(D.to_host(el)[0]),
                    local_count=sum(piece_count(pc) for pc in pieces))
 
 
@@ -435,11 +435,11 @@ def run_3way_nccl(problem, grid, stages, keep_values: bool = True) -> Outcome:
     start.record()
     r.step()
     end.record()
-    end.synchronize()
+    D.spin_event(end)
     el = torch.tensor([start.elapsed_time(end) * 1e-3], dtype=torch.float64, device=r.dev)
     dist.all_reduce(el, op=dist.ReduceOp.MAX)
     lo, hi, deg, cnt = r.totals()
-    return Outcome(r.pieces, lo, hi, deg, cnt, r.global_sums(), float(el.item()),
+    return Outcome(r.pieces, lo, hi, deg, cnt, r.global_sums(), float(D.to_host(el)[0]),
                    local_count=r.count)
 
 

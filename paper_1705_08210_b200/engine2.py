@@ -81,7 +81,9 @@ class HostSink:
         dev.record_stream(self.stream)
 
     def finish(self) -> None:
-        self.stream.synchronize()
+        ev = torch.cuda.Event()
+        ev.record(self.stream)
+        D.spin_event(ev)
 
 
 def run_task(code: int, problem, grid, task: Task2, row_blocks: list, col_blocks: list,
@@ -221,10 +223,10 @@ def run_streamed(problem, host: torch.Tensor, keep_values: bool, sink) -> Outcom
     D.raise_on_flags(flags)  # DataError like VectorBlock (core.py:239-242)
     _mark("checked")
     end.record()
-    end.synchronize()
+    D.spin_event(end)
     lo, hi, deg = D.acc_words(acc)
     piece = PairPiece(0, 0, n, n, True, 0, n, vals)
-    return Outcome([piece], lo, hi, deg, count, sums.cpu().numpy(),
+    return Outcome([piece], lo, hi, deg, count, D.to_host(sums),
                    start.elapsed_time(end) * 1e-3)
 
 
@@ -296,11 +298,11 @@ def run_local(problem, grid, balance: str = "split", keep_values: bool = True,
     for k in range(0, len(specs), 16):
         D.czek2_tasks(code, specs[k:k + 16], problem.n_v, acc)
     end.record()
-    end.synchronize()
+    D.spin_event(end)
     if sink is not None:
         sink.finish()
     lo, hi, deg = D.acc_words(acc)
-    all_sums = torch.cat([sums[p] for p in range(grid.n_pv)]).cpu().numpy()
+    all_sums = D.to_host(torch.cat([sums[p] for p in range(grid.n_pv)]))
     return Outcome(pieces, lo, hi, deg, count, all_sums, start.elapsed_time(end) * 1e-3)
 
 

@@ -218,11 +218,11 @@ def run_local(problem, grid, stages, keep_values: bool = True,
                 count += run_boxes_field(code, problem, merge_boxes(boxes), slab_blocks, sums,
                                          tables, acc, keep_values, pieces)
     end.record()
-    end.synchronize()
+    D.spin_event(end)
     if sink is not None:
         sink.finish()
     lo, hi, deg = D.acc_words(acc)
-    all_sums = torch.cat([sums[p] for p in range(grid.n_pv)]).cpu().numpy()
+    all_sums = D.to_host(torch.cat([sums[p] for p in range(grid.n_pv)]))
     return Outcome(pieces, lo, hi, deg, count, all_sums, start.elapsed_time(end) * 1e-3)
 
 
@@ -390,7 +390,7 @@ class Runner3Dist:
         return Checksum128.from_words(lo, hi).hex
 
     def global_sums(self):
-        return torch.cat([self.sums[s] for s in range(self.grid.n_pv)]).cpu().numpy()
+        return D.to_host(torch.cat([self.sums[s] for s in range(self.grid.n_pv)]))
 
     def teardown(self) -> None:
         for name in ("blocks", "sums", "tables", "acc", "buf", "pieces"):
