@@ -85,8 +85,6 @@ def main():
                                       "segment.all.allocated", 0) - m0.get("segment.all.allocated", 0),
                                   "trace_ms": {b[0]: round(a[1].elapsed_time(b[1]), 3) for a, b in
                                                zip(engine2.LAST_TRACE, engine2.LAST_TRACE[1:])},
-                                  "flag_trace_ms": [(n, round((t - engine2.LAST_TRACE[-2][2]) * 1e3, 3))
-                                                    for n, t in D.HOST_TRACE],
                                   "host_trace_ms": {b[0]: round((b[2] - a[2]) * 1e3, 3) for a, b in
                                                     zip(engine2.LAST_TRACE,
                                                         engine2.LAST_TRACE[1:])},
