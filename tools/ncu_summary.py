@@ -71,7 +71,10 @@ def main():
                 continue
             op = re.sub(r"^@!?U?P\w+\s+", "", r[ix["Source"]].strip()).split(" ")[0].split(".")[0]
             for c in cols:
-                v = int(r[ix[c]] or 0)
+                try:
+                    v = int(r[ix[c]] or 0)
+                except ValueError:  # a second kernel's header row / non-numeric cell
+                    continue
                 by[op][c] += v
                 tot += v
         print("Stall samples by SASS opcode (share of all samples; top reasons):\n")
