@@ -206,8 +206,10 @@ class Runner2:
         self.problem, self.grid, self.balance, self.keep = problem, grid, balance, keep_values
         self.sink = HostSink() if host_values else None
         # fused: the diagonal task runs while every block exchange is in flight,
-        # then all remaining tasks of the slab share one grid (no per-task tail)
-        self.fused = grid.n_pf == 1 and not host_values
+        # then all remaining tasks of the slab share one grid (no per-task tail);
+        # host values go zero-copy into pinned buffers (banded copies need the
+        # per-task path)
+        self.fused = grid.n_pf == 1 and (self.sink is None or self.sink.direct)
         self.coords = coords_of_rank(self.rank, grid)
         self.code = D.code_of(problem.precision)
         self.n_vp = problem.n_v // grid.n_pv
@@ -277,8 +279,11 @@ class Runner2:
             specs = []
             for t, (V, s_col) in zip(ts, blocks):
                 m, n = t.r1 - t.r0, t.c1 - t.c0
-                vals = torch.empty(D.pair_count(m, n, t.diagonal), dtype=tdt,
-                                   device=self.dev) if self.keep else None
+                cnt = D.pair_count(m, n, t.diagonal)
+                if self.sink is not None:  # zero-copy: the epilogue writes pinned host memory
+                    vals = self.sink.buffer(cnt, tdt)
+                else:
+                    vals = torch.empty(cnt, dtype=tdt, device=self.dev) if self.keep else None
                 specs.append((self.own, t.r0, t.r1, V, t.c0, t.c1, s_own, s_col, t.diagonal,
                               vals))
                 pieces.append(PairPiece(self.own.v0 + t.r0, V.v0 + t.c0, m, n, t.diagonal, 0, m,

@@ -21,6 +21,35 @@ import torch.distributed as dist  # noqa: E402
 import paper_1705_08210_b200 as P  # noqa: E402
 
 
+def check_host_values(world, rank) -> int:
+    """run_2way(transport="nccl", host_values=True): every rank's values land in
+    pinned host memory (zero-copy from the fused multi-task grids); the values
+    each rank holds, with their canonical indices, must re-checksum to the
+    global checksum, which must equal the local single-GPU run's."""
+    from oracle import propsim_np as O  # test infrastructure: the checker
+
+    prob = P.Problem(2, 900, 16 * world + 8, P.gen_uniform(77, 900, 16 * world + 8), "double")
+    grid = P.DecompGrid(n_pv=world)
+    res = P.run_2way(prob, grid, transport="nccl", host_values=True)
+    idx = res.records.canonical_indices()
+    vals = res.records.values
+    part = O.checksum(idx, vals) if len(idx) else 0
+    t = torch.tensor([part & ((1 << 63) - 1), (part >> 63) & ((1 << 63) - 1), part >> 126],
+                     dtype=torch.int64, device="cuda")
+    allp = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(allp, t)
+    total = sum(int(a[0]) | (int(a[1]) << 63) | (int(a[2]) << 126) for a in allp) % (1 << 128)
+    bad = 0
+    if rank == 0:
+        want = P.run_2way(prob, grid).checksum.hex
+        ok = res.checksum.hex == want and format(total, "032x") == want
+        bad = int(not ok)
+        print(json.dumps({"case": "nccl host_values", "n_v": prob.n_v, "grid": {"n_pv": world},
+                          "checksum": res.checksum.hex, "rechecked": format(total, "032x"),
+                          "want": want, "ok": ok}), flush=True)
+    return bad
+
+
 def main():
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -75,6 +104,7 @@ def main():
             print(json.dumps({"arity": c["arity"], "precision": c["precision"], "n_f": c["n_f"],
                               "n_v": c["n_v"], "grid": c["grid"], "checksum": res.checksum.hex,
                               "want": want, "ok": ok, "elapsed": res.elapsed}), flush=True)
+    bad += check_host_values(world, rank)
     bad += check_outputs(gold, world, rank)
     t = torch.tensor([bad], device="cuda")
     dist.broadcast(t, 0)
