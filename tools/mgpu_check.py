@@ -31,7 +31,7 @@ def check_host_values(world, rank) -> int:
     prob = P.Problem(2, 900, 16 * world + 8, P.gen_uniform(77, 900, 16 * world + 8), "double")
     grid = P.DecompGrid(n_pv=world)
     res = P.run_2way(prob, grid, transport="nccl", host_values=True)
-    idx = res.records.canonical_indices()
+    idx = res.records.canonical_indices
     vals = res.records.values
     part = O.checksum(idx, vals) if len(idx) else 0
     t = torch.tensor([part & ((1 << 63) - 1), (part >> 63) & ((1 << 63) - 1), part >> 126],
