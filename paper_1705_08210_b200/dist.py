@@ -27,6 +27,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
+from . import _native as N
 from . import device as D
 from .domain import ConfigError, RankCoords, coords_of_rank, n_ranks, rank_of_coords
 from .engine2 import HostSink, Outcome, finish_numerators, run_task
@@ -237,7 +238,20 @@ class Runner2:
     def setup(self) -> None:
         dev = torch.device("cuda", torch.cuda.current_device())
         self.dev = dev
-        self.own = D.load_block(self.problem, self.grid, self.coords, dev)
+        # a pinned host slab (end-to-end use) is uploaded in chunks during the
+        # step, overlapped with the diagonal task (_step_streamed)
+        self.host, self.flags = None, None
+        if self.fused and os.environ.get("PSIM_STREAMED", "1") != "0":
+            from .engine2 import pinned_host_block
+
+            self.host = pinned_host_block(self.problem, self.grid, self.coords)
+        if self.host is not None:
+            n_fp = self.problem.n_f // self.grid.n_pf
+            data = D.alloc_block(n_fp, self.n_vp, self.problem.precision, dev)
+            self.own = D.Block(data, n_fp, self.n_vp, data.shape[1], self.coords.p_v * self.n_vp,
+                               self.problem.precision)
+        else:
+            self.own = D.load_block(self.problem, self.grid, self.coords, dev)
         # receive buffers: fused mode keeps every received block (all exchanges
         # in flight at once, one multi-task grid after them); otherwise one per
         # in-flight exchange (double buffering). None without a vector split.
@@ -307,10 +321,87 @@ class Runner2:
         self.s_own = s_own
         return events
 
+    def _step_streamed(self, timed: bool) -> list:
+        """Fused step with the own block still in pinned host memory: the
+        diagonal task is the streamed kernel (psim_czek2_streamed: the copy
+        engine uploads the block in chunks while the kernel starts on the
+        tiles whose vectors have landed); the column sums, the device-side
+        validation and every block exchange are queued on the copy stream
+        behind the upload, so NCCL ships the block as soon as it is in HBM
+        while the diagonal task computes; the remaining tasks form one grid."""
+        import ctypes as C
+
+        from .engine2 import copy_stream, stream_chunk
+
+        p = self.problem
+        tdt = D.torch_dtype(p.precision)
+        own, n = self.own, self.n_vp
+        copy = copy_stream(self.dev)
+        copy.wait_stream(torch.cuda.current_stream())  # buffers of the previous step are free
+        chunk = stream_chunk(n)
+        bm, _ = N.tile_shape(self.code)
+        ready = torch.empty(-(-n // chunk) + -(-n // bm), dtype=torch.int32, device=self.dev)
+        s_kernel = torch.empty(n, dtype=tdt, device=self.dev)  # written by the streamed kernel
+        cnt = D.pair_count(n, n, True)
+        if self.sink is not None:
+            vals = self.sink.buffer(cnt, tdt)  # zero-copy host output
+        else:
+            vals = torch.empty(cnt, dtype=tdt, device=self.dev) if self.keep else None
+        t = N.Block2(W=own.data.data_ptr(), ldw=own.ld, V=own.data.data_ptr(), ldv=own.ld,
+                     n_f=own.n_fp, m=n, n=n, diagonal=1, g_row=own.v0, g_col=own.v0, n_v=p.n_v,
+                     vals=D.ptr(vals), acc=self.acc.data_ptr(), s_row=s_kernel.data_ptr())
+        events = []
+        if timed:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+        N.call("psim_czek2_streamed", self.code, C.byref(t), self.host.data_ptr(), own.n_fp, chunk,
+               ready.data_ptr(), D.stream_ptr(), copy.cuda_stream)
+        if timed:
+            e1.record()
+            events.append((e0, e1))
+        exchanges = [e for e in self.events if isinstance(e, Exchange)]
+        slot_of, works = {}, []
+        with torch.cuda.stream(copy):  # behind the upload
+            s_own = D.column_sums(own)  # == the kernel's sums, bit for bit (k_colsum order)
+            self.flags = D.check_values_async(own.data, own.n_fp, n, own.ld, self.code)
+            for k, ev in enumerate(exchanges):
+                slot_of[ev.step] = k
+                self.remote[k].v0 = ((self.coords.p_v + ev.step) % self.grid.n_pv) * self.n_vp
+                works.extend(self._post_exchange(ev, k, s_own))
+        for w in works:
+            w.wait()
+        torch.cuda.current_stream().wait_stream(copy)
+        pieces = [PairPiece(own.v0, own.v0, n, n, True, 0, n, vals)]
+        rest = [e for e in self.events if isinstance(e, Task2) and not e.diagonal]
+        specs = []
+        for tk in rest:
+            V, s_col = self.remote[slot_of[tk.step]], self.remote_sums[slot_of[tk.step]]
+            m2, n2 = tk.r1 - tk.r0, tk.c1 - tk.c0
+            c2 = D.pair_count(m2, n2, False)
+            if self.sink is not None:
+                v2 = self.sink.buffer(c2, tdt)
+            else:
+                v2 = torch.empty(c2, dtype=tdt, device=self.dev) if self.keep else None
+            specs.append((own, tk.r0, tk.r1, V, tk.c0, tk.c1, s_own, s_col, False, v2))
+            pieces.append(PairPiece(own.v0 + tk.r0, V.v0 + tk.c0, m2, n2, False, 0, m2, v2))
+        if specs:
+            if timed:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+            D.czek2_tasks(self.code, specs, p.n_v, self.acc)
+            if timed:
+                e1.record()
+                events.append((e0, e1))
+        self.pieces = pieces
+        self.s_own = s_own
+        return events
+
     def step(self, timed: bool = False) -> list:
         """Run this rank's whole plan once; returns (start, end) kernel events."""
         p, g = self.problem, self.grid
         self.acc.zero_()
+        if self.host is not None:
+            return self._step_streamed(timed)
         s_own = self._sums()
         if self.fused:
             return self._step_fused(s_own, timed)
@@ -422,6 +513,9 @@ def run_2way_nccl(problem, grid, balance: str = "split", keep_values: bool = Tru
     D.spin_event(end)
     if r.sink is not None:
         r.sink.finish()
+    if r.flags is not None:  # streamed input, validated on the device: every rank raises
+        dist.all_reduce(r.flags)
+        D.raise_on_flags(r.flags)
     el = torch.tensor([start.elapsed_time(end) * 1e-3], dtype=torch.float64, device=r.dev)
     dist.all_reduce(el, op=dist.ReduceOp.MAX)
     lo, hi, deg, cnt = r.totals()

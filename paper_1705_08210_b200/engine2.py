@@ -143,9 +143,9 @@ def finish_numerators(code, N, r0, r1, m, n, diagonal, s_row, s_col, g_row, g_co
 _COPY_STREAM: dict = {}
 
 
-def pinned_host_block(problem, grid):
-    """The single-slab block as a pinned (n_v, n_f) host tensor when the
-    source hands out pinned memory (no copy), else None."""
+def pinned_host_block(problem, grid, coords=None):
+    """A rank's block (default: the single slab) as a pinned (n_vp, n_fp) host
+    tensor when the source hands out pinned memory (no copy), else None."""
     import os
 
     from .domain import host_block
@@ -157,7 +157,7 @@ def pinned_host_block(problem, grid):
         return None
     if synthetic_kind(src) is not None or is_vector_file(src):
         return None
-    arr = host_block(problem, grid, RankCoords(0, 0, 0))  # (n_f, n_v) Fortran
+    arr = host_block(problem, grid, coords or RankCoords(0, 0, 0))  # (n_fp, n_vp) Fortran
     host = torch.from_numpy(np.ascontiguousarray(arr.T))  # (n_v, n_f), same bytes
     return host if host.is_pinned() else None
 
@@ -179,6 +179,18 @@ def _mark(name: str) -> None:
         LAST_TRACE.append((name, ev, time.perf_counter()))
 
 
+def copy_stream(dev) -> torch.cuda.Stream:
+    """The per-device side stream the streamed inputs are uploaded on."""
+    if dev.index not in _COPY_STREAM:
+        _COPY_STREAM[dev.index] = torch.cuda.Stream(device=dev)
+    return _COPY_STREAM[dev.index]
+
+
+def stream_chunk(n: int) -> int:
+    """Vectors per upload chunk of a streamed block (<= 64 chunks)."""
+    return max(256, -(-n // 64))
+
+
 def run_streamed(problem, host: torch.Tensor, keep_values: bool, sink) -> Outcome:
     """Single-slab run whose input is still in pinned host memory: the copy
     engine uploads the block in chunks (last vectors first) while the fused
@@ -192,14 +204,14 @@ def run_streamed(problem, host: torch.Tensor, keep_values: bool, sink) -> Outcom
     code = D.code_of(problem.precision)
     n_f, n = problem.n_f, problem.n_v
     tdt = D.torch_dtype(problem.precision)
-    copy = _COPY_STREAM.setdefault(dev.index, torch.cuda.Stream(device=dev))
+    copy = copy_stream(dev)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     LAST_TRACE.clear()
     start.record()
     _mark("start")
     data = D.alloc_block(n_f, n, problem.precision, dev)
     ld = data.shape[1]
-    chunk = max(256, -(-n // 64))
+    chunk = stream_chunk(n)
     bm, _ = N.tile_shape(code)
     ready = torch.empty(-(-n // chunk) + -(-n // bm), dtype=torch.int32, device=dev)
     sums = torch.empty(n, dtype=tdt, device=dev)  # written by the kernel

@@ -28,8 +28,25 @@ def check_host_values(world, rank) -> int:
     global checksum, which must equal the local single-GPU run's."""
     from oracle import propsim_np as O  # test infrastructure: the checker
 
-    prob = P.Problem(2, 900, 16 * world + 8, P.gen_uniform(77, 900, 16 * world + 8), "double")
+    n_v = 300 * world + 40
+    gen = P.Problem(2, 900, n_v, P.gen_uniform(77, 900, n_v), "double")
     grid = P.DecompGrid(n_pv=world)
+    # this rank's slab in pinned host memory: the streamed-input NCCL path
+    from paper_1705_08210_b200 import device as D
+    from paper_1705_08210_b200.domain import coords_of_rank
+
+    coords = coords_of_rank(rank, grid)
+    blk = D.load_block(gen, grid, coords, torch.device("cuda"))
+    host = torch.empty((blk.n_vp, blk.n_fp), dtype=blk.data.dtype, pin_memory=True)
+    host.copy_(blk.data[:, :blk.n_fp])
+    torch.cuda.synchronize()
+
+    class Slab:
+        def local_block(self, problem, grid_, coords_):
+            assert tuple(coords_) == tuple(coords)
+            return host.numpy().T
+
+    prob = P.Problem(2, 900, n_v, Slab(), "double")
     res = P.run_2way(prob, grid, transport="nccl", host_values=True)
     idx = res.records.canonical_indices
     vals = res.records.values
@@ -41,7 +58,7 @@ def check_host_values(world, rank) -> int:
     total = sum(int(a[0]) | (int(a[1]) << 63) | (int(a[2]) << 126) for a in allp) % (1 << 128)
     bad = 0
     if rank == 0:
-        want = P.run_2way(prob, grid).checksum.hex
+        want = P.run_2way(gen, grid).checksum.hex
         ok = res.checksum.hex == want and format(total, "032x") == want
         bad = int(not ok)
         print(json.dumps({"case": "nccl host_values", "n_v": prob.n_v, "grid": {"n_pv": world},
