@@ -364,7 +364,11 @@ __device__ __forceinline__ void minplus_tile(const typename C::T* __restrict__ W
     const T* As = st;
     const T* Bs = st + C::BM * C::PITCH;
     // (the 3-way pivot loop keeps the full unroll: rolled it measured 2% slower)
+#ifdef PSIM_PIVOT_KKU
+    constexpr int U = PIVOT ? PSIM_PIVOT_KKU : C::KKU;
+#else
     constexpr int U = PIVOT ? C::BK / C::VEC : C::KKU;
+#endif
 #pragma unroll U
     for (int kk = 0; kk < C::BK; kk += C::VEC) micro_step<C>(acc, As, Bs, ty, tx, kk);
   }
