@@ -502,24 +502,43 @@ class Runner2:
         torch.cuda.empty_cache()
 
 
+# PSIM_TRACE=1: host perf_counter marks of run_2way_nccl (tools/exp_e2e_nccl.py)
+LAST_TRACE: list = []
+
+
+def _mark(name: str) -> None:
+    if os.environ.get("PSIM_TRACE") == "1":
+        import time
+
+        LAST_TRACE.append((name, time.perf_counter()))
+
+
 def run_2way_nccl(problem, grid, balance: str = "split", keep_values: bool = True,
                   host_values: bool = False) -> Outcome:
+    LAST_TRACE.clear()
+    _mark("enter")
     r = Runner2(problem, grid, balance, keep_values, host_values)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record()
     r.setup()
+    _mark("setup")
     r.step()
+    _mark("step")
     end.record()
     D.spin_event(end)
+    _mark("device")
     if r.sink is not None:
         r.sink.finish()
     if r.flags is not None:  # streamed input, validated on the device: every rank raises
         dist.all_reduce(r.flags)
         D.raise_on_flags(r.flags)
+    _mark("flags")
     el = torch.tensor([start.elapsed_time(end) * 1e-3], dtype=torch.float64, device=r.dev)
     dist.all_reduce(el, op=dist.ReduceOp.MAX)
     lo, hi, deg, cnt = r.totals()
+    _mark("totals")
     sums = r.global_sums()
+    _mark("sums")
     pieces = r.pieces
     return Outcome(pieces, lo, hi, deg, cnt, sums, float(D.to_host(el)[0]),
                    local_count=sum(piece_count(pc) for pc in pieces))

@@ -44,7 +44,9 @@ def main():
             return host.numpy().T
 
     prob = P.Problem(2, n_f, n_v, Slab(), "double")
-    for rep in range(4):
+    os.environ["PSIM_TRACE"] = "1"
+    from paper_1705_08210_b200 import dist as PD
+    for rep in range(6):
         dist.barrier()
         torch.cuda.synchronize()
         st = (C.c_uint64 * 4)()
@@ -52,10 +54,15 @@ def main():
         t0 = time.perf_counter()
         res = P.run_2way(prob, grid, transport="nccl", host_values=True)
         wall = time.perf_counter() - t0
+        lead = (PD.LAST_TRACE[0][1] - t0) * 1e3 if PD.LAST_TRACE else None
         N.call("psim_stream_stats", st, 1)
-        print(json.dumps({"rank": rank, "rep": rep, "wall_s": round(wall, 4),
+        print(json.dumps({"rank": rank, "rep": rep, "wall_s": round(wall, 4), "lead_ms": lead,
                           "device_s": round(res.elapsed, 4),
                           "chunk_wait_sm_ms": st[0] / 1e6, "max_wait_ms": st[3] / 1e6,
+                          "trace_ms": {b[0]: round((b[1] - a[1]) * 1e3, 2) for a, b in
+                                       zip(PD.LAST_TRACE, PD.LAST_TRACE[1:])},
+                          "tail_ms": round((time.perf_counter() - PD.LAST_TRACE[-1][1]) * 1e3, 2)
+                          if PD.LAST_TRACE else None,
                           "checksum": res.checksum.hex}), flush=True)
         del res
     dist.destroy_process_group()
