@@ -155,6 +155,16 @@ def to_host(t: torch.Tensor) -> np.ndarray:
     return host.numpy()
 
 
+def to_device(values, dtype, dev) -> torch.Tensor:
+    """A small host list as a device tensor without a blocking copy (pinned
+    staging + an asynchronous upload; cf. spin_event). CPU devices (gloo
+    tests) get a plain tensor."""
+    if torch.device(dev).type != "cuda":
+        return torch.tensor(values, dtype=dtype, device=dev)
+    host = torch.tensor(values, dtype=dtype).pin_memory()
+    return host.to(dev, non_blocking=True)
+
+
 def raise_on_flags(flags: torch.Tensor) -> None:
     bad, neg = (int(x) for x in to_host(flags))
     if bad:

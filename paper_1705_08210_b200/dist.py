@@ -103,7 +103,7 @@ def piece_count(pc) -> int:
 
 def gather_totals(acc: torch.Tensor, count: int, world: int, dev) -> tuple[int, int, int, int]:
     """All-gather every rank's (checksum lo, hi, degenerate, count); sum mod 2^128."""
-    mine = torch.tensor([*D.to_host(acc).tolist(), count], dtype=torch.int64, device=dev)
+    mine = D.to_device([*D.to_host(acc).tolist(), count], torch.int64, dev)
     allv = torch.empty(world * 4, dtype=torch.int64, device=dev)
     dist.all_gather_into_tensor(allv, mine)
     allv = allv.view(world, 4)
@@ -533,7 +533,7 @@ def run_2way_nccl(problem, grid, balance: str = "split", keep_values: bool = Tru
         dist.all_reduce(r.flags)
         D.raise_on_flags(r.flags)
     _mark("flags")
-    el = torch.tensor([start.elapsed_time(end) * 1e-3], dtype=torch.float64, device=r.dev)
+    el = D.to_device([start.elapsed_time(end) * 1e-3], torch.float64, r.dev)
     dist.all_reduce(el, op=dist.ReduceOp.MAX)
     lo, hi, deg, cnt = r.totals()
     _mark("totals")
@@ -554,7 +554,7 @@ def run_3way_nccl(problem, grid, stages, keep_values: bool = True) -> Outcome:
     r.step()
     end.record()
     D.spin_event(end)
-    el = torch.tensor([start.elapsed_time(end) * 1e-3], dtype=torch.float64, device=r.dev)
+    el = D.to_device([start.elapsed_time(end) * 1e-3], torch.float64, r.dev)
     dist.all_reduce(el, op=dist.ReduceOp.MAX)
     lo, hi, deg, cnt = r.totals()
     return Outcome(r.pieces, lo, hi, deg, cnt, r.global_sums(), float(D.to_host(el)[0]),

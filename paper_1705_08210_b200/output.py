@@ -286,10 +286,12 @@ def _allreduce_count(result) -> int:
     import torch
     import torch.distributed as dist
 
+    from . import device as D
+
     dev = _comm_device()
-    t = torch.tensor([len(result.records)], dtype=torch.int64, device=dev)
+    t = D.to_device([len(result.records)], torch.int64, dev)
     dist.all_reduce(t)
-    return int(t.item())
+    return int(D.to_host(t)[0])
 
 
 # ---------------------------------------------------------------------------

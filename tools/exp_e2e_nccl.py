@@ -46,7 +46,7 @@ def main():
     prob = P.Problem(2, n_f, n_v, Slab(), "double")
     os.environ["PSIM_TRACE"] = "1"
     from paper_1705_08210_b200 import dist as PD
-    for rep in range(6):
+    for rep in range(int(os.environ.get("REPS", "6"))):
         dist.barrier()
         torch.cuda.synchronize()
         st = (C.c_uint64 * 4)()
