@@ -16,7 +16,7 @@ import torch
 
 from . import _native as N
 from . import device as D
-from .domain import ConfigError, RankCoords
+from .domain import RankCoords
 from .engine2 import Outcome, fold_sums
 from .plan import Box, Unit3, merge_boxes, plan_3way, unit_boxes
 from .records import BoxPiece
