@@ -13,7 +13,9 @@ compaction / checksum kernel(s), all values written to HBM.
   the 126 MB L2, so no flush is needed between steps.
 * ``e2e``: the same metric through the public API (``run_2way`` with a
   pinned-host ArraySource-style source): H2D of the inputs, the run, and
-  D2H of every value + the checksum inside the timed region.
+  D2H of every value + the checksum inside the timed region. 3-way configs:
+  ``run_3way`` from the pinned slab with the checksum read back (cfg4's
+  288 GB of values exceed host memory).
 * ``roofline``: the dominant kernel's achieved cmp/s over its launch time
   vs the min+add issue peak microbenchmarked in the same process
   (psim_peak_minplus).
@@ -22,7 +24,8 @@ compaction / checksum kernel(s), all values written to HBM.
   host threads over a bounded sample of the same workload.
 
 N > 1 runs under torchrun: the config's vector axis is split over N slabs
-(circulant plan, NCCL send/recv of blocks), same total work ("strong").
+(circulant 2-way / tetrahedral 3-way plan, NCCL send/recv of blocks; cfg5
+splits the field axis), same total work ("strong").
 """
 from __future__ import annotations
 
