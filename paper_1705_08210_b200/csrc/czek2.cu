@@ -12,6 +12,8 @@
 // so the next task's CTAs fill SMs as the previous grid drains and the tasks
 // share one tail. Tasks never read each other's outputs (their checksum terms
 // meet only in commutative atomics), so no dependent waits.
+#include <cstdlib>
+
 #include "minplus.cuh"
 #include "psim_internal.h"
 
@@ -23,7 +25,12 @@ enum Mode2 : int {
   kRawPacked = 2,  // numerators in the packed value layout (triangle or row-major rectangle)
   kCzek2Streamed = 3,  // kCzek2 while the block is still arriving: tiles bottom-up, each
                        // waits for its input chunk's ready flag; sums computed in the tile
+  kCzek2Flat = 4,  // kCzek2 over several off-diagonal tasks of the same rows laid end to
+                   // end along the columns (segments): one ragged column tile per group
+                   // instead of one per task; a tile may straddle two segments
 };
+
+constexpr int kMaxSeg = 16;  // segments of a kCzek2Flat launch (each >= BN columns)
 
 template <typename T>
 struct Args2 {
@@ -49,7 +56,24 @@ struct Args2 {
   int64_t chunk;              // kCzek2Streamed: vectors per chunk
   T* sums;                    // kCzek2Streamed: column sums, published per row tile
   unsigned* sum_ready;        // kCzek2Streamed: sum_ready[r] != 0 once row tile r's are in
+  // kCzek2Flat: segment s is flat columns [seg_c0[s], seg_c0[s+1]) = columns of
+  // task s, read from seg_V[s] (stride ldv), sums seg_scol[s], global ids from
+  // seg_gcol[s], values to seg_out[s] (row-major, seg_c0[s+1]-seg_c0[s] wide)
+  int nseg;
+  int64_t seg_c0[kMaxSeg + 1];
+  const T* seg_V[kMaxSeg];
+  const T* seg_scol[kMaxSeg];
+  int64_t seg_gcol[kMaxSeg];
+  T* seg_out[kMaxSeg];
 };
+
+// Segment of flat column c (kCzek2Flat): a short uniform scan.
+template <typename T>
+__device__ __forceinline__ int seg_of(const Args2<T>& a, int64_t c) {
+  int s = 0;
+  while (s + 1 < a.nseg && a.seg_c0[s + 1] <= c) ++s;
+  return s;
+}
 
 // kCzek2Streamed: the host uploads the block in chunks from the LAST vector
 // down (copy engine, flag after each chunk), so a tile whose lowest vector is
@@ -186,9 +210,21 @@ __global__ void __launch_bounds__(kNT, C::MINB) k_minplus2(const Args2<typename 
       if (threadIdx.x == 0) wait_ready(a.ready + min64(row0, col0) / a.chunk, 0);
       __syncthreads();
     }
-    minplus_tile<C, false>(a.W + row0 * a.ldw, a.ldw, (int)min64(C::BM, a.m_end - row0),
-                           a.V + col0 * a.ldv, a.ldv, (int)min64(C::BN, a.n - col0), nullptr,
-                           a.n_f, acc, smem);
+    if constexpr (MODE == kCzek2Flat) {
+      // columns [col0, split) from segment s, the rest from segment s + 1
+      const int s = seg_of(a, col0);
+      const int cols = (int)min64(C::BN, a.n - col0);
+      const int split = (int)min64(cols, a.seg_c0[s + 1] - col0);
+      const T* V1 = a.seg_V[s] + (col0 - a.seg_c0[s]) * a.ldv;
+      const T* V2b = split < cols ? a.seg_V[s + 1] - (int64_t)split * a.ldv : V1;
+      minplus_tile<C, false, false, true>(a.W + row0 * a.ldw, a.ldw,
+                                          (int)min64(C::BM, a.m_end - row0), V1, a.ldv, cols,
+                                          nullptr, a.n_f, acc, smem, nullptr, V2b, split);
+    } else {
+      minplus_tile<C, false>(a.W + row0 * a.ldw, a.ldw, (int)min64(C::BM, a.m_end - row0),
+                             a.V + col0 * a.ldv, a.ldv, (int)min64(C::BN, a.n - col0), nullptr,
+                             a.n_f, acc, smem);
+    }
   }
   // the tile is decoded again rather than kept live across the mainloop
   band_tile(tb, a.row_pref, a.nbands, a.band, a.row_tile0, a.row_tile0 + a.tiles_m, C::BM, C::BN,
@@ -207,7 +243,37 @@ __global__ void __launch_bounds__(kNT, C::MINB) k_minplus2(const Args2<typename 
     __syncthreads();
   }
   const int ty = thread_ty(), tx = thread_tx();
-  if (MODE == kCzek2 || STREAMED) {
+  if constexpr (MODE == kCzek2Flat) {
+    const int s1 = seg_of(a, col0);
+    const int64_t cb = a.seg_c0[s1 + 1];  // first flat column of segment s1 + 1
+    Cks c;
+#pragma unroll
+    for (int mi = 0; mi < C::TM; ++mi) {
+      const int li = ty + 16 * mi;
+      if (li >= rows) continue;
+      const int64_t i = row0 + li;
+      const T si = a.s_row[i];
+      const uint64_t gi = (uint64_t)(a.g_row + i);
+#pragma unroll
+      for (int nj = 0; nj < C::TN; ++nj) {
+        const int lj = tx + 16 * nj;
+        if (lj >= cols) continue;
+        const int64_t jf = col0 + lj;
+        const int s = jf >= cb ? s1 + 1 : s1;
+        const int64_t j = jf - a.seg_c0[s];
+        const T d = Traits<T>::add(si, a.seg_scol[s][j]);
+        const bool zero = (d == T(0));
+        const T v = zero ? T(0) : Traits<T>::div(Traits<T>::mul(T(2), acc[mi][nj]), d);
+        T* out = a.seg_out[s];
+        if (out) out[i * (a.seg_c0[s + 1] - a.seg_c0[s]) + j] = v;
+        const uint64_t gj = (uint64_t)(a.seg_gcol[s] + j);
+        const uint64_t gidx = gi < gj ? pair_index(gi, gj, a.n_v) : pair_index(gj, gi, a.n_v);
+        c.term(gidx, Traits<T>::bits(v));
+        c.deg += zero ? 1ull : 0ull;
+      }
+    }
+    cks_block_flush<kNT>(a.acc, c);
+  } else if (MODE == kCzek2 || STREAMED) {
     Cks c;
 #pragma unroll
     for (int mi = 0; mi < C::TM; ++mi) {
@@ -332,8 +398,13 @@ template <class C, int MODE>
 static cudaError_t launch_group(Args2<typename C::T>* args, const int64_t* row_begin,
                                 const int64_t* row_end, int count, cudaStream_t st) {
   constexpr int smem_bytes = C::SMEM_BYTES;
+  // a kCzek2 group may hold flattened tasks (nseg > 0): those run k_minplus2<C, kCzek2Flat>
+  constexpr int FLAT_MODE = MODE == kCzek2 ? kCzek2Flat : MODE;
   cudaError_t e = cudaFuncSetAttribute(k_minplus2<C, MODE>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+  if (e == cudaSuccess && FLAT_MODE != MODE)
+    e = cudaFuncSetAttribute(k_minplus2<C, FLAT_MODE>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
   if (e != cudaSuccess) return e;
   int64_t total_bands = 0;
   int64_t* blocks = new int64_t[count];
@@ -368,7 +439,8 @@ static cudaError_t launch_group(Args2<typename C::T>* args, const int64_t* row_b
     attr[0].val.programmaticStreamSerializationAllowed = first ? 0 : 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, k_minplus2<C, MODE>, args[k]);
+    e = args[k].nseg > 0 ? cudaLaunchKernelEx(&cfg, k_minplus2<C, FLAT_MODE>, args[k])
+                         : cudaLaunchKernelEx(&cfg, k_minplus2<C, MODE>, args[k]);
     first = false;
   }
   delete[] blocks;
@@ -394,6 +466,59 @@ static Args2<T> make_args(const void* W, int64_t ldw, const void* V, int64_t ldv
   return a;
 }
 
+// Off-diagonal tasks over the same rows (same W, sums, global row ids, whole
+// row range) and field layout are merged, in order, into one kCzek2Flat task
+// whose columns are theirs laid end to end: the group has one ragged column
+// tile instead of one per task (a task of 5000 vectors fills 39 of its 40
+// column tiles with 8/128 of the last). Each segment must be >= BN wide, so a
+// tile touches at most two. Values, record layout and checksum terms are those
+// of the separate tasks. PSIM_NO_FLAT=1 disables it (A/B).
+template <class C>
+static int flatten_tasks(Args2<typename C::T>* args, int64_t* rb, int64_t* re, int ntasks) {
+  static const bool off = [] {
+    const char* v = getenv("PSIM_NO_FLAT");
+    return v && v[0] == '1';
+  }();
+  if (off) return ntasks;
+  auto eligible = [&](int k) {
+    const auto& a = args[k];
+    return !a.diagonal && rb[k] == 0 && re[k] == 0 && a.n >= C::BN && a.m > 0;
+  };
+  auto same_rows = [&](int k, int l) {
+    const auto& a = args[k];
+    const auto& b = args[l];
+    return a.W == b.W && a.ldw == b.ldw && a.m == b.m && a.n_f == b.n_f && a.ldv == b.ldv &&
+           a.s_row == b.s_row && a.g_row == b.g_row && a.n_v == b.n_v && a.acc == b.acc;
+  };
+  int out = 0;
+  for (int k = 0; k < ntasks;) {
+    int l = k + 1;
+    if (eligible(k))
+      while (l < ntasks && l - k < kMaxSeg && eligible(l) && same_rows(k, l)) ++l;
+    Args2<typename C::T> a = args[k];
+    if (l - k > 1) {
+      a.nseg = l - k;
+      int64_t c = 0;
+      for (int s = 0; s < a.nseg; ++s) {
+        const auto& t = args[k + s];
+        a.seg_c0[s] = c;
+        a.seg_V[s] = t.V;
+        a.seg_scol[s] = t.s_col;
+        a.seg_gcol[s] = t.g_col;
+        a.seg_out[s] = t.out;
+        c += t.n;
+      }
+      a.seg_c0[a.nseg] = c;
+      a.n = c;
+    }
+    rb[out] = rb[k];
+    re[out] = re[k];
+    args[out++] = a;
+    k = l;
+  }
+  return out;
+}
+
 template <typename T>
 cudaError_t czek2_tasks_t(const Czek2Block* tasks, int ntasks, cudaStream_t st) {
   Args2<T>* args = new Args2<T>[ntasks];
@@ -412,7 +537,8 @@ cudaError_t czek2_tasks_t(const Czek2Block* tasks, int ntasks, cudaStream_t st) 
     rb[k] = t.row_begin;
     re[k] = t.row_end;
   }
-  cudaError_t e = launch_group<typename Prod<T>::C, kCzek2>(args, rb, re, ntasks, st);
+  const int count = flatten_tasks<typename Prod<T>::C>(args, rb, re, ntasks);
+  cudaError_t e = launch_group<typename Prod<T>::C, kCzek2>(args, rb, re, count, st);
   delete[] args;
   delete[] rb;
   delete[] re;

@@ -189,13 +189,16 @@ __device__ __forceinline__ void micro_step(uint32_t (&acc)[C::TM][C::TN], const 
 }
 
 // Stage field chunk kt of `rows` W vectors and `cols` V vectors (and, with
-// PIVOT, of the pivot column) into stage buffer `st`.
-template <class C, bool PIVOT>
+// PIVOT, of the pivot column) into stage buffer `st`. TWO: the tile's columns
+// come from two blocks -- columns >= split are read from V2b + col * ldv
+// (V2b = the second block's first vector minus split vectors).
+template <class C, bool PIVOT, bool TWO = false>
 __device__ __forceinline__ void stage_load(typename C::T* st, const typename C::T* __restrict__ W,
                                            int64_t ldw, int rows,
                                            const typename C::T* __restrict__ V, int64_t ldv,
                                            int cols, const typename C::T* __restrict__ xj,
-                                           int64_t n_f, int kt) {
+                                           int64_t n_f, int kt,
+                                           const typename C::T* V2b = nullptr, int split = 0) {
   using T = typename C::T;
   const int tid = threadIdx.x;
   const int64_t q_base = (int64_t)kt * C::BK;
@@ -218,7 +221,9 @@ __device__ __forceinline__ void stage_load(typename C::T* st, const typename C::
     const int64_t rem = (n_f - q0) * (int64_t)sizeof(T);
     int bytes = rem >= 16 ? 16 : (rem > 0 ? (int)rem : 0);
     const T* src = V;
-    if (row < cols && bytes) src = V + row * ldv + q0; else bytes = 0;
+    const T* vb = V;
+    if constexpr (TWO) vb = row < split ? V : V2b;
+    if (row < cols && bytes) src = vb + row * ldv + q0; else bytes = 0;
     cp_async16(st + (C::BM + row) * C::PITCH + ch * C::VEC, src, bytes);
   }
 }
@@ -280,14 +285,15 @@ __device__ __forceinline__ int thread_tx() {
 // SUMS: thread t < BM + BN also folds the column sum of tile vector t (rows,
 // then columns) from the staged chunks -- sequential ascending q from +0,
 // the order of k_colsum, so the sum is bit-identical -- into *vsum.
-template <class C, bool PIVOT, bool SUMS = false>
+template <class C, bool PIVOT, bool SUMS = false, bool TWO = false>
 __device__ __forceinline__ void minplus_tile(const typename C::T* __restrict__ W, int64_t ldw,
                                              int rows, const typename C::T* __restrict__ V,
                                              int64_t ldv, int cols,
                                              const typename C::T* __restrict__ xj, int64_t n_f,
                                              typename C::T (&acc)[C::TM][C::TN],
                                              typename C::T* smem,
-                                             typename C::T* vsum = nullptr) {
+                                             typename C::T* vsum = nullptr,
+                                             const typename C::T* V2b = nullptr, int split = 0) {
   using T = typename C::T;
   using V4 = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
   constexpr int S = C::STAGES;
@@ -309,7 +315,8 @@ __device__ __forceinline__ void minplus_tile(const typename C::T* __restrict__ W
 #pragma unroll
   for (int s = 0; s < S - 1; ++s) {
     if (s < KT) {
-      stage_load<C, PIVOT>(smem + s * C::STAGE_ELEMS, W, ldw, rows, V, ldv, cols, xj, n_f, s);
+      stage_load<C, PIVOT, TWO>(smem + s * C::STAGE_ELEMS, W, ldw, rows, V, ldv, cols, xj, n_f,
+                                s, V2b, split);
       if (PIVOT) pivot_load<C>(smem + s * C::STAGE_ELEMS, xj, n_f, s);
     }
     cp_async_commit();
@@ -340,8 +347,8 @@ __device__ __forceinline__ void minplus_tile(const typename C::T* __restrict__ W
     }
     const int nk = kt + S - 1;
     if (nk < KT) {
-      stage_load<C, PIVOT>(smem + (nk % S) * C::STAGE_ELEMS, W, ldw, rows, V, ldv, cols, xj,
-                           n_f, nk);
+      stage_load<C, PIVOT, TWO>(smem + (nk % S) * C::STAGE_ELEMS, W, ldw, rows, V, ldv, cols,
+                                xj, n_f, nk, V2b, split);
       if (PIVOT) pivot_load<C>(smem + (nk % S) * C::STAGE_ELEMS, xj, n_f, nk);
     }
     cp_async_commit();

@@ -494,3 +494,30 @@ def test_streamed_capi_validation():
     rc = lib.psim_czek2_streamed(N.F64, C.byref(t), pageable.ctypes.data, 20, 4,
                                  ready.data_ptr(), s1.cuda_stream, s2.cuda_stream)
     assert rc == 1
+
+
+@pytest.mark.parametrize("precision", ["double", "single"])
+def test_flattened_offdiagonal_tasks_bitwise_vs_oracle(precision):
+    """Blocks wider than a column tile: a rank's off-diagonal circulant tasks
+    run as one kCzek2Flat task (columns end to end, tiles straddling two
+    blocks; czek2.cu flatten_tasks). n_vp = 500 / 375 / 300 / 250 covers full
+    tasks, split half-blocks wider (187) and narrower (125) than BN, which stay
+    separate. Identical bits and checksum to the sequential oracle, with and
+    without kept values."""
+    from oracle import propsim_np as O
+
+    P = _api()
+    n_f, n_v = 257, 1500
+    dt = np.float64 if precision == "double" else np.float32
+    want, _ = O.values_2way(O.uniform(5, n_f, n_v, dt))
+    cks = O.checksum_hex(np.arange(len(want)), want)
+    for n_pv in (3, 4, 5, 6):
+        prob = P.Problem(2, n_f, n_v, P.gen_uniform(5, n_f, n_v), precision)
+        res = P.run_2way(prob, P.DecompGrid(n_pv=n_pv))
+        assert (res.records.values.view(np.uint8) == want.view(np.uint8)).all(), n_pv
+        assert res.checksum.hex == cks, n_pv
+        res = P.run_2way(prob, P.DecompGrid(n_pv=n_pv), keep_values=False)
+        assert res.checksum.hex == cks, n_pv
+    res = P.run_2way(prob, P.DecompGrid(n_pv=5), host_values=True)
+    assert (res.records.values.view(np.uint8) == want.view(np.uint8)).all()
+    assert res.checksum.hex == cks
