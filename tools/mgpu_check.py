@@ -84,6 +84,9 @@ def main():
     # extra grids checked against the local single-GPU run
     extra = [
         (2, "double", 1000, 240, dict(n_pv=world)),
+        # blocks wider than a column tile: flattened off-diagonal tasks (kCzek2Flat)
+        (2, "double", 300, 330 * world, dict(n_pv=world)),
+        (2, "single", 200, 200 * world + 8, dict(n_pv=world)),
         (2, "single", 3000, 400, dict(n_pf=world)),
         (2, "double", 777, 120, dict(n_pr=world)),
         (3, "double", 300, 12 * world, dict(n_pv=world)),
