@@ -394,22 +394,29 @@ static int64_t plan2(Args2<typename C::T>& a, int64_t row_begin, int64_t row_end
 
 // Launch a group of tasks (same mode): band prefixes first, then the grids
 // back to back, each after the first as a programmatic dependent launch.
-template <class C, int MODE>
+// Tasks with edge[k] run the 32-row edge configuration CE.
+template <class C, int MODE, class CE = C>
 static cudaError_t launch_group(Args2<typename C::T>* args, const int64_t* row_begin,
-                                const int64_t* row_end, int count, cudaStream_t st) {
-  constexpr int smem_bytes = C::SMEM_BYTES;
+                                const int64_t* row_end, int count, cudaStream_t st,
+                                const bool* edge = nullptr) {
   // a kCzek2 group may hold flattened tasks (nseg > 0): those run k_minplus2<C, kCzek2Flat>
   constexpr int FLAT_MODE = MODE == kCzek2 ? kCzek2Flat : MODE;
-  cudaError_t e = cudaFuncSetAttribute(k_minplus2<C, MODE>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
-  if (e == cudaSuccess && FLAT_MODE != MODE)
-    e = cudaFuncSetAttribute(k_minplus2<C, FLAT_MODE>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+  cudaError_t e = cudaSuccess;
+  {
+    static_assert(std::is_same<typename C::T, typename CE::T>::value, "one element type");
+    void* const kerns[4] = {(void*)k_minplus2<C, MODE>, (void*)k_minplus2<C, FLAT_MODE>,
+                            (void*)k_minplus2<CE, MODE>, (void*)k_minplus2<CE, FLAT_MODE>};
+    const int smem[4] = {C::SMEM_BYTES, C::SMEM_BYTES, CE::SMEM_BYTES, CE::SMEM_BYTES};
+    for (int q = 0; q < 4 && e == cudaSuccess; ++q)
+      e = cudaFuncSetAttribute(kerns[q], cudaFuncAttributeMaxDynamicSharedMemorySize, smem[q]);
+  }
   if (e != cudaSuccess) return e;
+  auto is_edge = [&](int k) { return edge != nullptr && edge[k]; };
   int64_t total_bands = 0;
   int64_t* blocks = new int64_t[count];
   for (int k = 0; k < count; ++k) {
-    blocks[k] = plan2<C>(args[k], row_begin ? row_begin[k] : 0, row_end ? row_end[k] : 0);
+    const int64_t rb = row_begin ? row_begin[k] : 0, re = row_end ? row_end[k] : 0;
+    blocks[k] = is_edge(k) ? plan2<CE>(args[k], rb, re) : plan2<C>(args[k], rb, re);
     if (MODE == kCzek2Streamed && blocks[k] > 0) blocks[k] += args[k].tiles_m;  // sum CTAs
     if (blocks[k] > 0x7fffffffLL) e = cudaErrorInvalidConfiguration;
     if (blocks[k] > 0) total_bands += args[k].nbands + 1;
@@ -422,8 +429,9 @@ static cudaError_t launch_group(Args2<typename C::T>* args, const int64_t* row_b
     Args2<typename C::T>& a = args[k];
     a.row_pref = pref + off;
     off += a.nbands + 1;
-    k_band_prefix<<<1, 1024, 0, st>>>(a.nbands, a.band, a.row_tile0, a.tiles_m, a.tiles_n,
-                                      C::BM, C::BN, a.diagonal, pref + (a.row_pref - pref));
+    const int64_t bm = is_edge(k) ? CE::BM : C::BM, bn = is_edge(k) ? CE::BN : C::BN;
+    k_band_prefix<<<1, 1024, 0, st>>>(a.nbands, a.band, a.row_tile0, a.tiles_m, a.tiles_n, bm,
+                                      bn, a.diagonal, pref + (a.row_pref - pref));
     e = cudaGetLastError();
   }
   bool first = true;
@@ -432,15 +440,20 @@ static cudaError_t launch_group(Args2<typename C::T>* args, const int64_t* row_b
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)blocks[k]);
     cfg.blockDim = dim3(kNT);
-    cfg.dynamicSmemBytes = smem_bytes;
+    cfg.dynamicSmemBytes = is_edge(k) ? CE::SMEM_BYTES : C::SMEM_BYTES;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = first ? 0 : 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    e = args[k].nseg > 0 ? cudaLaunchKernelEx(&cfg, k_minplus2<C, FLAT_MODE>, args[k])
-                         : cudaLaunchKernelEx(&cfg, k_minplus2<C, MODE>, args[k]);
+    const bool flat = args[k].nseg > 0;
+    if (is_edge(k))
+      e = flat ? cudaLaunchKernelEx(&cfg, k_minplus2<CE, FLAT_MODE>, args[k])
+               : cudaLaunchKernelEx(&cfg, k_minplus2<CE, MODE>, args[k]);
+    else
+      e = flat ? cudaLaunchKernelEx(&cfg, k_minplus2<C, FLAT_MODE>, args[k])
+               : cudaLaunchKernelEx(&cfg, k_minplus2<C, MODE>, args[k]);
     first = false;
   }
   delete[] blocks;
@@ -537,8 +550,46 @@ cudaError_t czek2_tasks_t(const Czek2Block* tasks, int ntasks, cudaStream_t st) 
     rb[k] = t.row_begin;
     re[k] = t.row_end;
   }
-  const int count = flatten_tasks<typename Prod<T>::C>(args, rb, re, ntasks);
-  cudaError_t e = launch_group<typename Prod<T>::C, kCzek2>(args, rb, re, count, st);
+  using C = typename Prod<T>::C;
+  using CE = typename Edge<T>::C;
+  const int count = flatten_tasks<C>(args, rb, re, ntasks);
+  // The ragged last row tile of each task (rows past the last multiple of BM)
+  // runs as an edge task with 32-row tiles at the end of the chain, where its
+  // small CTAs also fill the tail. PSIM_NO_EDGE=1 disables it (A/B).
+  static const bool no_edge = [] {
+    const char* v = getenv("PSIM_NO_EDGE");
+    return v && v[0] == '1';
+  }();
+  Args2<T>* all = new Args2<T>[2 * count];
+  int64_t* arb = new int64_t[2 * count];
+  int64_t* are = new int64_t[2 * count];
+  bool* edge = new bool[2 * count];
+  int n_all = 0;
+  for (int k = 0; k < count; ++k) {
+    const int64_t m_end = re[k] > 0 ? re[k] : args[k].m;
+    const int64_t full = rb[k] + (m_end - rb[k]) / C::BM * C::BM;
+    const bool split = !no_edge && full < m_end;
+    if (!split || full > rb[k]) {
+      all[n_all] = args[k];
+      arb[n_all] = rb[k];
+      are[n_all] = split ? full : re[k];
+      edge[n_all++] = false;
+    }
+  }
+  for (int k = 0; k < count; ++k) {
+    const int64_t m_end = re[k] > 0 ? re[k] : args[k].m;
+    const int64_t full = rb[k] + (m_end - rb[k]) / C::BM * C::BM;
+    if (no_edge || full >= m_end) continue;
+    all[n_all] = args[k];
+    arb[n_all] = full;
+    are[n_all] = m_end;
+    edge[n_all++] = true;
+  }
+  cudaError_t e = launch_group<C, kCzek2, CE>(all, arb, are, n_all, st, edge);
+  delete[] all;
+  delete[] arb;
+  delete[] are;
+  delete[] edge;
   delete[] args;
   delete[] rb;
   delete[] re;

@@ -80,6 +80,19 @@ struct Prod<float> {
   using C = Cfg<float, 8, 4, 3, 2, 1>;  // 128 x 64, 2 CTAs/SM, scalar FADD
 };
 
+// Edge configurations: 32-row tiles for the last, ragged row tile of a 2-way
+// task (a 5000-vector block leaves 8 rows in its 40th 128-row tile).
+template <typename T>
+struct Edge;
+template <>
+struct Edge<double> {
+  using C = Cfg<double, 2, 8, 4, 2, 0>;  // 32 x 128
+};
+template <>
+struct Edge<float> {
+  using C = Cfg<float, 2, 4, 3, 4, 1>;  // 32 x 64
+};
+
 // FP32 packed add: two independent accumulators, each rounded exactly as a
 // scalar __fadd_rn (add.rn.f32x2 keeps subnormals; no .ftz).
 __device__ __forceinline__ void fadd2(float& a0, float& a1, float x0, float x1) {
