@@ -140,7 +140,11 @@ int psim_mgemm(int dtype, const void* W, int64_t ldw, const void* V, int64_t ldv
 int psim_czek2_block(int dtype, const psim_block2_t* task, void* stream);
 /* Several tasks of one rank (same dtype, n_f, n_v) in a single grid, so the
  * circulant steps of a slab share one launch and one tail (metrics2.py:148-158
- * over the plan of schedule.py:116-142). */
+ * over the plan of schedule.py:116-142). Consecutive off-diagonal tasks over
+ * the same rows (same W, s_row, g_row, whole row range, each >= one column
+ * tile wide) are computed as one task with their columns end to end, and each
+ * task's rows past its last multiple of 128 as a 32-row-tile edge task; the
+ * values each task writes and its checksum terms do not change. */
 int psim_czek2_tasks(int dtype, const psim_block2_t* tasks, int ntasks, void* stream);
 /* pack_bits (mingemm.py:279-291): 32 fields per uint32 word, bit q%32 of
  * word q/32 of vector i at words[i * ldw + q/32] (ldw % 4 == 0, padding
