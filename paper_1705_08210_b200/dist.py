@@ -196,6 +196,21 @@ def allgather_ops(me: int, n_pv: int, blocks: dict, sums: dict, peer) -> list:
     return ops
 
 
+
+def _task_grids(tasks, bn: int) -> int:
+    """Grids psim_czek2_tasks launches for ``tasks`` (each with a band prefix):
+    consecutive full-row off-diagonal tasks >= bn wide are merged
+    (czek2.cu flatten_tasks), and a task whose rows are not a multiple of 128
+    adds a 32-row edge grid."""
+    groups = []
+    for t in tasks:
+        ok = not t.diagonal and t.r0 == 0 and t.c1 - t.c0 >= bn
+        if ok and groups and groups[-1][0] and groups[-1][1] == t.r1 and len(groups[-1][2]) < 16:
+            groups[-1][2].append(t)
+        else:
+            groups.append((ok, t.r1, [t]))
+    return sum(1 + int((r1 - g[0].r0) % 128 != 0) for _, r1, g in groups)
+
 class Runner2:
     """One rank's 2-way pipeline over NCCL (also the multi-GPU bench harness)."""
 
@@ -224,7 +239,10 @@ class Runner2:
         # a field split runs per task min-plus + (n_pf - 1) folds + epilogue
         if self.fused:
             grids = int(any(t.diagonal for t in tasks)) + int(any(not t.diagonal for t in tasks))
-            self.launches_per_step = 1 + grids
+            diag = [t for t in tasks if t.diagonal]
+            rest = [t for t in tasks if not t.diagonal]
+            bn = 128 if problem.precision == "double" else 64
+            self.launches_per_step = 1 + 2 * (_task_grids(diag, bn) + _task_grids(rest, bn))
         else:
             grids = len(tasks)
             per_task = 1 if grid.n_pf == 1 else 1 + (grid.n_pf - 1) + 1

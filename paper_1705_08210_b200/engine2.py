@@ -334,8 +334,10 @@ class Resident2:
             raise ValueError("Resident2 runs a single-rank grid")
         self.problem, self.grid = problem, grid
         self.code = D.code_of(problem.precision)
-        self.launches_per_step = 2  # column sums, fused min-plus kernel
         n = problem.n_v
+        # column sums, then per task a band prefix + the fused min-plus grid:
+        # the 128-row task and, when n_v % 128 != 0, its 32-row edge task
+        self.launches_per_step = 1 + 2 * (1 + int(n % 128 != 0))
         self.kernel_cmp_per_launch = problem.n_f * (n * (n - 1) // 2)
 
     def setup(self) -> None:
