@@ -11,7 +11,9 @@
 // programmatic dependent launch: every CTA signals launch_dependents on entry,
 // so the next task's CTAs fill SMs as the previous grid drains and the tasks
 // share one tail. Tasks never read each other's outputs (their checksum terms
-// meet only in commutative atomics), so no dependent waits.
+// meet only in commutative atomics), so no dependent waits. Off-diagonal tasks
+// over the same rows run as one column-flattened task (kCzek2Flat), and each
+// task's ragged last row tile as a 32-row edge task (czek2_tasks_t).
 #include <cstdlib>
 
 #include "minplus.cuh"
