@@ -557,7 +557,9 @@ cudaError_t czek2_tasks_t(const Czek2Block* tasks, int ntasks, cudaStream_t st) 
   const int count = flatten_tasks<C>(args, rb, re, ntasks);
   // The ragged last row tile of each task (rows past the last multiple of BM)
   // runs as an edge task with 32-row tiles at the end of the chain, where its
-  // small CTAs also fill the tail. PSIM_NO_EDGE=1 disables it (A/B).
+  // small CTAs also fill the tail -- when it has at most 3 * 32 rows: a 32-row
+  // tile issues at ~85% of the full tile's rate, so 4 of them cost more than
+  // one 128-row tile. PSIM_NO_EDGE=1 disables it (A/B).
   static const bool no_edge = [] {
     const char* v = getenv("PSIM_NO_EDGE");
     return v && v[0] == '1';
@@ -570,7 +572,7 @@ cudaError_t czek2_tasks_t(const Czek2Block* tasks, int ntasks, cudaStream_t st) 
   for (int k = 0; k < count; ++k) {
     const int64_t m_end = re[k] > 0 ? re[k] : args[k].m;
     const int64_t full = rb[k] + (m_end - rb[k]) / C::BM * C::BM;
-    const bool split = !no_edge && full < m_end;
+    const bool split = !no_edge && full < m_end && m_end - full <= 3 * CE::BM;
     if (!split || full > rb[k]) {
       all[n_all] = args[k];
       arb[n_all] = rb[k];
@@ -581,7 +583,7 @@ cudaError_t czek2_tasks_t(const Czek2Block* tasks, int ntasks, cudaStream_t st) 
   for (int k = 0; k < count; ++k) {
     const int64_t m_end = re[k] > 0 ? re[k] : args[k].m;
     const int64_t full = rb[k] + (m_end - rb[k]) / C::BM * C::BM;
-    if (no_edge || full >= m_end) continue;
+    if (no_edge || full >= m_end || m_end - full > 3 * CE::BM) continue;
     all[n_all] = args[k];
     arb[n_all] = full;
     are[n_all] = m_end;

@@ -200,8 +200,8 @@ def allgather_ops(me: int, n_pv: int, blocks: dict, sums: dict, peer) -> list:
 def _task_grids(tasks, bn: int) -> int:
     """Grids psim_czek2_tasks launches for ``tasks`` (each with a band prefix):
     consecutive full-row off-diagonal tasks >= bn wide are merged
-    (czek2.cu flatten_tasks), and a task whose rows are not a multiple of 128
-    adds a 32-row edge grid."""
+    (czek2.cu flatten_tasks), and a task whose rows end 1..96 past a multiple
+    of 128 adds a 32-row edge grid."""
     groups = []
     for t in tasks:
         ok = not t.diagonal and t.r0 == 0 and t.c1 - t.c0 >= bn
@@ -209,7 +209,7 @@ def _task_grids(tasks, bn: int) -> int:
             groups[-1][2].append(t)
         else:
             groups.append((ok, t.r1, [t]))
-    return sum(1 + int((r1 - g[0].r0) % 128 != 0) for _, r1, g in groups)
+    return sum(1 + int(0 < (r1 - g[0].r0) % 128 <= 96) for _, r1, g in groups)
 
 class Runner2:
     """One rank's 2-way pipeline over NCCL (also the multi-GPU bench harness)."""

@@ -336,8 +336,8 @@ class Resident2:
         self.code = D.code_of(problem.precision)
         n = problem.n_v
         # column sums, then per task a band prefix + the fused min-plus grid:
-        # the 128-row task and, when n_v % 128 != 0, its 32-row edge task
-        self.launches_per_step = 1 + 2 * (1 + int(n % 128 != 0))
+        # the 128-row task and, when n_v % 128 is 1..96, its 32-row edge task
+        self.launches_per_step = 1 + 2 * (1 + int(0 < n % 128 <= 96))
         self.kernel_cmp_per_launch = problem.n_f * (n * (n - 1) // 2)
 
     def setup(self) -> None:

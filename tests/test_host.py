@@ -195,7 +195,7 @@ def test_checksum_host_utility_kat():
 def test_fused_launch_count_follows_flattening(n_pv):
     """dist._task_grids mirrors psim_czek2_tasks: consecutive full-row
     off-diagonal tasks >= BN wide share one grid, split half-row tasks do not,
-    and a row count off a multiple of 128 adds one 32-row edge grid."""
+    and a row count 1..96 past a multiple of 128 adds one 32-row edge grid."""
     from paper_1705_08210_b200.dist import _task_grids
 
     n_vp = 5000  # 39 * 128 + 8: every task has an edge grid
@@ -211,3 +211,5 @@ def test_fused_launch_count_follows_flattening(n_pv):
         want = 2 * (int(bool(full_rows)) + len(half_rows))
         assert _task_grids(rest, 128) == want, (p, [(t.r0, t.r1, t.c0, t.c1) for t in rest])
     assert _task_grids([], 128) == 0
+    t = PL.Task2(0, 0, 0, 0, 128 + 100, 0, 128 + 100)  # 100 ragged rows: one 128-row tile
+    assert _task_grids([t], 128) == 1
