@@ -149,7 +149,16 @@ def comparisons(arity, n_f, n_v) -> int:
 # CPU baseline: the C port of the reference's blocked kernel on all host threads
 
 
-def cpu_baseline(arity, precision, n_f, target_s: float = 12.0) -> dict:
+def cpu_baseline(arity, precision, n_f, bits, target_s: float = 12.0) -> dict:
+    """The reference's single-rank run_2way (metrics2.py:108-171: dense
+    numerator of the diagonal block by the blocked kernel, column sums, the
+    value of every pair and the 128-bit checksum) restated in C
+    (oracle/psim_oracle.c oracle_czek2_*), on all host threads, over a
+    bounded sample of the workload: the config's n_f and dtype, n_v sized
+    to take about ``target_s`` seconds. A 3-way comparison is one min-plus
+    step as well (metrics3.py:161-169 runs the same blocked kernel), so the
+    same sample measures the CPU's comparison rate for both arities.
+    The rate is extrapolated to the full config (``extrapolated``)."""
     from oracle import c_oracle
     from oracle import propsim_np as O
 
@@ -157,26 +166,63 @@ def cpu_baseline(arity, precision, n_f, target_s: float = 12.0) -> dict:
     dt = np.float64 if precision == "double" else np.float32
     nth = c_oracle.threads()
     nf = min(n_f, 250000)
-    # calibrate on a small slice, then size a ~target_s sample
-    W = O.random_exact(SEED, nf, 4096, 6, dt, v0=0, v1=256)
+    # calibrate on a small run, then size the sample
+    V = O.random_exact(SEED, nf, 1 << 20, bits, dt, v0=0, v1=256)
     t0 = time.perf_counter()
-    c_oracle.mgemm(W, W, nth)
+    c_oracle.czek2(V, nth)
     rate0 = nf * 256 * 256 / (time.perf_counter() - t0)
     side = int(math.sqrt(max(rate0 * target_s / nf, 256 * 256)))
     side = max(256, min(side, 16384)) // 128 * 128
-    W = O.random_exact(SEED, nf, 1 << 20, 6, dt, v0=0, v1=side)
+    V = O.random_exact(SEED, nf, 1 << 20, bits, dt, v0=0, v1=side)
     t0 = time.perf_counter()
-    c_oracle.mgemm(W, W, nth)
+    _, cks, _ = c_oracle.czek2(V, nth)
     el = time.perf_counter() - t0
-    rate = nf * side * side / el
-    if arity == 3:  # a 3-way comparison is one min-plus step of the pivot kernel
-        pass
+    # unique pairs are the reference's metric (cli.py:244); the dense
+    # diagonal block it computes to get them is its cost
+    rate = nf * math.comb(side, 2) / el
+    t0 = time.perf_counter()
+    c_oracle.mgemm(V, V, nth)
+    el_k = time.perf_counter() - t0
     return {
         "value": rate, "unit": "comparisons/s", "cores": nth, "kind": "port",
-        "sample": f"oracle/psim_oracle.c blocked min-plus (mingemm.py:94-117 restated), "
-                  f"{precision}, n_f={nf} x {side}x{side} outputs, {nth} threads, {el:.1f} s; "
-                  f"kernel rate, records/checksum excluded",
+        "extrapolated": True, "sample_wall_s": el,
+        "sample": f"oracle/psim_oracle.c full single-rank run_2way (metrics2.py:108-171 "
+                  f"restated: dense blocked min-plus mingemm.py:94-117, column sums, every "
+                  f"pair value, 128-bit checksum), {precision}, n_f={nf} x n_v={side} "
+                  f"({math.comb(side, 2)} pairs), {nth} threads, {el:.1f} s; rate "
+                  f"extrapolated to the full config",
+        "kernel_only": {"value": nf * side * side / el_k, "unit": "comparisons/s",
+                        "seconds": el_k,
+                        "sample": f"blocked min-plus alone, {side}x{side} dense outputs"},
+        "sample_checksum": cks,
     }
+
+
+def cpu_cfg1_end_to_end(expect: str | None) -> dict:
+    """cfg1 (2-way FP64, 1000 x 500, seed 2026,
+    bits 20) run whole by the C restatement of the reference's single-rank
+    run_2way on all host threads; its checksum must equal the reference's
+    (SURVEY Appendix B, ea23ebab...) and the GPU's."""
+    from oracle import c_oracle
+    from oracle import propsim_np as O
+
+    V = O.random_exact(SEED, 1000, 500, 20)
+    nth = c_oracle.threads()
+    c_oracle.czek2(V, nth)
+    times = []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        _, cks, _ = c_oracle.czek2(V, nth)
+        times.append(time.perf_counter() - t0)
+    el = statistics.median(times)
+    return {"workload": CONFIGS["cfg1"][5], "seconds": el,
+            "value": 1000 * math.comb(500, 2) / el, "unit": "comparisons/s", "cores": nth,
+            "checksum": cks, "checksum_matches_reference": cks == CFG1_REFERENCE_CHECKSUM,
+            "checksum_matches_gpu": (cks == expect) if expect else None}
+
+
+# SURVEY Appendix B / tests/golden/golden.json: the reference's own cfg1 checksum
+CFG1_REFERENCE_CHECKSUM = "ea23ebab734aeaaefdc87babae741b72"
 
 
 # ---------------------------------------------------------------------------
@@ -257,18 +303,23 @@ def run_ours(args) -> dict | None:
     kernel_ms = []
     with sampler:
         barrier()
+        N.launch_count(reset=True)
         ev0.record(st)
         for _ in range(args.steps):
             kernel_ms.extend(runner.step(timed=True))
         ev1.record(st)
+        launches = N.launch_count()  # libpsim's own count of the kernels it launched
         barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    launches = runner.launches_per_step * args.steps
+        t = torch.tensor([ms, launches], device=dev, dtype=torch.float64)
+        dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)  # whole job: every rank's launches
+        ms, launches = float(t[0].item()), int(t[1].item())
     cks = runner.checksum_hex()
+    # checker (after the timed region): sampled tuples recomputed from their
+    # columns alone by the oracle (SURVEY 8d "Parity at full size")
+    parity = sampled_parity(runner, prob, bits, world, dev) if not args.no_parity else None
 
     # dominant kernel: algorithmic comparisons per launch over its event time
     kern_cmp = runner.kernel_cmp_per_launch
@@ -335,15 +386,113 @@ def run_ours(args) -> dict | None:
             },
             "clocks": clocks,
             "gpu_launches": launches,
+            "gpu_launches_source": "psim_launch_count (libpsim counts every kernel it "
+                                   "launches) over the timed region, summed over ranks",
         }
+        if parity is not None:
+            line["parity"] = parity
         if e2e:
             line["e2e"] = e2e
         if not args.no_cpu:
-            line["cpu_baseline"] = cpu_baseline(arity, precision, n_f)
+            line["cpu_baseline"] = cpu_baseline(arity, precision, n_f, bits)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return line
+
+
+def sampled_parity(runner, prob, bits, world, dev) -> dict:
+    """Checker, run after the timed region: tuples of the benchmarked run
+    recomputed from their own columns by the oracle (SURVEY 8d "Parity at
+    full size": pair_numerators / column_sums / metric2_value, or the 3-way
+    triple recompute) and compared bit for bit with the values the kernels
+    wrote. 2-way: per value piece of this rank, a grid of sampled rows x
+    sampled columns (so ~10^4 pairs need only a few hundred generated
+    columns); 3-way: 300 triples of the last pivot chunk. Mismatches and
+    sample counts are summed over ranks."""
+    import torch
+
+    from oracle import propsim_np as O
+    from paper_1705_08210_b200 import device as D
+
+    dt = np.float64 if prob.precision == "double" else np.float32
+    n_f, n_v = prob.n_f, prob.n_v
+    rng = np.random.default_rng(7 + int(os.environ.get("RANK", "0")))
+    sampled = mismatches = 0
+    how = ""
+    if prob.arity == 2:
+        pieces = getattr(runner, "pieces", None)
+        if pieces is None:  # Resident2: one canonical single-slab piece
+            from paper_1705_08210_b200.records import PairPiece
+
+            pieces = [PairPiece(0, 0, n_v, n_v, True, 0, n_v, runner.vals)]
+        n_pf = getattr(getattr(runner, "grid", None), "n_pf", 1)
+        # sampled rows x sampled columns per piece; the recompute costs
+        # ~side^2 * n_f adds, so side shrinks with the field depth (cfg2:
+        # 160 x 160 -> ~1.2e4 pairs of the diagonal piece; cfg5: ~17 x 17)
+        side = int(math.sqrt(6e8 / n_f / max(1, len(pieces))))
+        side = max(8, min(160, side))
+        for pc in pieces:
+            if pc.values is None or pc.r1 <= pc.r0:
+                continue
+            rows = np.unique(np.concatenate([
+                rng.integers(pc.r0, pc.r1, size=side - 2), [pc.r0, pc.r1 - 1]]))
+            cols = np.unique(np.concatenate([rng.integers(0, pc.n, size=side - 2), [0, pc.n - 1]]))
+            VR = O.random_exact_cols(SEED, n_f, n_v, bits, pc.g_row + rows, dt)
+            VC = O.random_exact_cols(SEED, n_f, n_v, bits, pc.g_col + cols, dt)
+            want = O.pair_values_grid(VR, VC, n_pf)
+            li, lj = np.meshgrid(rows, cols, indexing="ij")
+            ok = (li < lj) if pc.diagonal else np.ones_like(li, dtype=bool)
+            li, lj, want = li[ok], lj[ok], want[ok]
+            if pc.diagonal:
+                pos = li * (2 * pc.m - li - 1) // 2 + (lj - li - 1)
+                base = pc.r0 * (2 * pc.m - pc.r0 - 1) // 2
+            else:
+                pos, base = li * pc.n + lj, pc.r0 * pc.n
+            idx = torch.as_tensor(pos - base, dtype=torch.int64, device=pc.values.device)
+            got = D.to_host(pc.values[idx])
+            mismatches += int((got.view(np.uint8).reshape(len(got), -1)
+                               != want.view(np.uint8).reshape(len(want), -1)).any(axis=1).sum())
+            sampled += len(got)
+        how = (f"per value piece: sampled rows x sampled columns ({side} each), values "
+               f"recomputed from their columns by oracle.propsim_np.pair_values_grid "
+               f"(n_pf={n_pf} ordered fold)")
+    elif hasattr(runner, "stage_boxes"):  # Resident3: the last pivot chunk is in runner.buf
+        from paper_1705_08210_b200.plan import box_count
+
+        box = runner.stage_boxes[-1][-1]
+        off, offs = 0, {}
+        for j in range(box.j0, box.j1):
+            offs[j] = off
+            off += max(0, min(box.i1, j) - box.i0) * max(0, box.k1 - max(box.k0, j + 1))
+        assert off == box_count(box)
+        triples = set()
+        while len(triples) < 300:
+            j = int(rng.integers(max(box.j0, 1), min(box.j1, n_v - 1)))
+            i = int(rng.integers(0, j))
+            k = int(rng.integers(j + 1, n_v))
+            triples.add((i, j, k))
+        triples = sorted(triples)
+        pos = [offs[j] + i * (n_v - j - 1) + (k - j - 1) for i, j, k in triples]
+        got = D.to_host(runner.buf[torch.as_tensor(pos, device=runner.buf.device)])
+        cols = sorted({c for t in triples for c in t})
+        at = {c: x for x, c in enumerate(cols)}
+        V = O.random_exact_cols(SEED, n_f, n_v, bits, cols, dt)
+        want = O.triple_values_sampled(V, [tuple(at[c] for c in t) for t in triples])
+        mismatches = int((got.view(np.uint8).reshape(len(got), -1)
+                          != want.view(np.uint8).reshape(len(want), -1)).any(axis=1).sum())
+        sampled = len(got)
+        how = ("300 triples of the last pivot chunk, recomputed from their three columns by "
+               "oracle.propsim_np.triple_values_sampled")
+    else:
+        return {"sampled": 0, "mismatches": 0, "note": "values not retained by this harness"}
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([sampled, mismatches], dtype=torch.int64, device=dev)
+        dist.all_reduce(t)
+        sampled, mismatches = int(t[0].item()), int(t[1].item())
+    return {"sampled": sampled, "mismatches": mismatches, "bitwise": True, "how": how}
 
 
 def e2e_2way(P, prob, grid, precision, args, total_cmp, world, rank) -> dict:
@@ -467,31 +616,102 @@ class SlabSource:
 
 
 def run_reference(args) -> dict | None:
+    """The reference arm: the reference's own CPU path restated in C
+    (oracle/psim_oracle.c; /root/reference is absent on the GPU box) on all
+    host threads. Each step is one full single-rank run_2way over a bounded
+    sample of the config (same n_f, dtype and bits; values + checksum
+    included); the rate is extrapolated to the full config. The line also
+    carries cfg1 run whole, checksum-checked."""
     world, rank, _ = dist_env()
     if rank != 0:
         return None
     arity, precision, n_f, n_v, bits, desc = CONFIGS[args.config]
     total = comparisons(arity, n_f, n_v)
-    rates = []
+    rates, walls = [], []
     base = None
-    for _ in range(max(1, args.warmup // 3)):
-        cpu_baseline(arity, precision, n_f, target_s=3.0)
+    cpu_baseline(arity, precision, n_f, bits, target_s=2.0)  # warm-up (build, page-in)
     for _ in range(max(1, min(args.steps, 3))):
-        base = cpu_baseline(arity, precision, n_f, target_s=10.0)
+        base = cpu_baseline(arity, precision, n_f, bits, target_s=10.0)
         rates.append(base["value"])
+        walls.append(base["sample_wall_s"])
     rate = statistics.median(rates)
     return {
         "impl": "reference",
-        "metric": METRIC, "value": rate, "unit": "comparisons/s", "n_gpus": world,
-        "steps": len(rates), "warmup": args.warmup, "ms_per_step": total / rate * 1e3,
+        "metric": METRIC, "value": rate, "unit": "comparisons/s", "n_gpus": args.gpus,
+        "steps": len(rates), "warmup": 1, "ms_per_step": statistics.median(walls) * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64" if precision == "double" else "f32",
-        "data": f"synthetic gen_random_exact(seed={SEED}) sample",
-        "config": {"workload": desc, "arity": arity, "num_field": n_f, "num_vector": n_v},
+        "data": f"synthetic gen_random_exact(seed={SEED}, bits={bits}) sample",
+        "extrapolated": True,
+        "extrapolated_full_step_s": total / rate,
+        "config": {"workload": desc, "arity": arity, "num_field": n_f, "num_vector": n_v,
+                   "sample": base["sample"]},
         "cpu_baseline": {**base, "value": rate},
+        "cfg1_end_to_end": cpu_cfg1_end_to_end(None),
         "e2e": {"value": rate, "unit": "comparisons/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
+
+
+def launch_check(args) -> dict | None:
+    """--launch-check: the rank plumbing of a bench run without a GPU (gloo):
+    every rank reports its rank / world and its slab's plan; rank 0 prints
+    them (tests/test_bench_launch.py runs ``bench.py --gpus 2 --launch-check``)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1705_08210_b200 import DecompGrid
+    from paper_1705_08210_b200.domain import coords_of_rank
+    from paper_1705_08210_b200.plan import Task2, plan_2way
+
+    world, rank, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    arity, precision, n_f, n_v, bits, desc = CONFIGS[args.config]
+    grid = DecompGrid(n_pf=world) if args.config == "cfg5" else DecompGrid(n_pv=world)
+    c = coords_of_rank(rank, grid)
+    tasks = [e for e in plan_2way(grid, c, n_v // grid.n_pv) if isinstance(e, Task2)]
+    mine = torch.tensor([rank, world, len(tasks)], dtype=torch.int64)
+    allv = [torch.zeros_like(mine) for _ in range(world)]
+    if world > 1:
+        dist.all_gather(allv, mine)
+        dist.destroy_process_group()
+    else:
+        allv = [mine]
+    if rank != 0:
+        return None
+    return {"launch_check": True, "n_gpus": world, "gpus_arg": args.gpus,
+            "parallelism": (f"field split n_pf={world}" if args.config == "cfg5" else
+                            f"circulant n_pv={world}"),
+            "ranks": [[int(x) for x in t.tolist()] for t in allv]}
+
+
+def self_launch(args) -> int | None:
+    """``--gpus N`` without a torchrun environment: re-launch this script as
+    N ranks (torch.distributed.run, 127.0.0.1) and return their exit code;
+    under torchrun, insist that the world size is N. NCCL's init lines
+    (communicator, ranks) go to stderr so every run shows its world."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is not None:
+        if int(world) != args.gpus and args.impl == "ours":
+            raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
+        return None
+    if args.gpus <= 1 or args.impl == "reference":
+        return None
+    import socket
+    import subprocess
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    log(f"[bench] self-launch: {' '.join(cmd)}")
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -505,14 +725,23 @@ def main():
     ap.add_argument("--n-f", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="CPU check of the multi-rank launch (gloo): print the world and plan")
     args = ap.parse_args()
+    rc = self_launch(args)
+    if rc is not None:
+        sys.exit(rc)
     # Keep stdout to the single JSON line: libraries (NCCL's version banner,
     # torch warnings) write to fd 1, so point fd 1 at stderr while running.
     sys.stdout.flush()
     saved = os.dup(1)
     os.dup2(2, 1)
     try:
-        line = run_reference(args) if args.impl == "reference" else run_ours(args)
+        if args.launch_check:
+            line = launch_check(args)
+        else:
+            line = run_reference(args) if args.impl == "reference" else run_ours(args)
     finally:
         sys.stdout.flush()
         os.dup2(saved, 1)

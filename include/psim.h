@@ -106,6 +106,10 @@ const char* psim_last_error(void);
 int psim_device_info(int* sm_count, int* cc_major, int* cc_minor);
 /* CTA output tile (rows x cols) of the min-plus kernels for a dtype. */
 int psim_tile_shape(int dtype, int* rows, int* cols);
+/* Kernel launches libpsim has issued in this process (all threads, all
+ * devices) since the last reset; reset != 0 returns the count and zeroes it.
+ * The benchmark's gpu_launches is this counter over the timed region. */
+int psim_launch_count(unsigned long long* out, int reset);
 
 /* --- inputs ---------------------------------------------------------------- */
 /* SyntheticSpec.local_block, kind "random-exact" (verify.py:126-147):
@@ -173,12 +177,16 @@ int psim_sorenson2_block(int dtype, const psim_block2_t* task, void* stream);
  * copy engine on copy_stream in chunks of `chunk` vectors from the last one
  * down, each followed by ready[c] = 1; the fused kernel on compute_stream
  * starts at the bottom tiles as soon as their chunk lands. The column sums
- * are folded in the mainloop of each row tile's first (diagonal) CTA, which
- * WRITES them to task->s_row (n entries, device) and publishes them with a
- * flag; task->s_col is not used. vals may be device or pinned host memory.
- * ready: device scratch of ceil(n / chunk) + ceil(n / BM) words (BM from
- * psim_tile_shape). The caller validates the block afterwards
- * (psim_check_block) and must keep `host` alive until copy_stream completes. */
+ * come from one extra CTA per row tile placed at the head of its bottom-up
+ * band: it folds its 128 vectors' sums (k_colsum's sequential order), WRITES
+ * them to task->s_row (n entries, device) and sets that row tile's
+ * sum-ready flag; the tile CTAs of the band wait on the flags of their rows
+ * and columns. task->s_col is not used. vals may be device or pinned host
+ * memory. ready: device scratch of ceil(n / chunk) + ceil(n / BM) words (BM
+ * from psim_tile_shape). A flag that does not arrive within 20 s makes the
+ * kernel give up instead of trapping: psim_stream_error then reports it. The
+ * caller validates the block afterwards (psim_check_block) and must keep
+ * `host` alive until copy_stream completes. */
 int psim_czek2_streamed(int dtype, const psim_block2_t* task, const void* host, int64_t host_ld,
                         int64_t chunk, unsigned* ready, void* compute_stream,
                         void* copy_stream);
@@ -186,6 +194,10 @@ int psim_czek2_streamed(int dtype, const psim_block2_t* task, const void* host, 
  * out4 = {ns tiles waited for input chunks, ns waited for column sums,
  * number of column-sum waits, longest single wait in ns}. */
 int psim_stream_stats(unsigned long long* out4, int reset);
+/* *aborted = 1 when the last streamed run gave up waiting for an input chunk
+ * or a column-sum flag (its results are invalid: raise EngineError); the
+ * flag is cleared by the next psim_czek2_streamed launch. Synchronous. */
+int psim_stream_error(unsigned* aborted);
 /* 2-way epilogue from reduced packed numerators, rows [r0, r1) of a task's
  * packed layout (field-axis path, metrics2.py:156-158). N and vals point at
  * the first entry of row r0. */

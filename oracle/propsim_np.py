@@ -279,6 +279,39 @@ def triple_values_sampled(V, triples, n_pf: int = 1):
     return out
 
 
+def _seq_sum_cols(X, slabs: int = 1):
+    """Per-column sequential ascending sums of X (n_f, k) from +0 (np.cumsum
+    along axis 0 is a strict left-to-right scan per column); with slabs > 1,
+    per-slab sums folded in ascending slab order (engine.py:197-216)."""
+    X = np.asarray(X)
+    w = X.shape[0] // slabs
+    total = None
+    for p in range(slabs):
+        part = np.cumsum(np.concatenate([np.zeros((1, X.shape[1]), X.dtype),
+                                         X[p * w:(p + 1) * w]]), axis=0)[-1]
+        total = part if total is None else total + part
+    return total
+
+
+def pair_values_grid(VR, VC, n_pf: int = 1):
+    """2-way values of every (row column r, col column c) combination,
+    recomputed from those columns only: pair_numerators (mingemm.py:237-247),
+    column_sums (212-222) and metric2_value (metrics2.py:77-82). Returns an
+    (a, b) array for VR (n_f, a) and VC (n_f, b)."""
+    VR, VC = np.asarray(VR), np.asarray(VC, dtype=np.asarray(VR).dtype)
+    dt = VR.dtype.type
+    sr, sc = _seq_sum_cols(VR, n_pf), _seq_sum_cols(VC, n_pf)
+    out = np.empty((VR.shape[1], VC.shape[1]), dtype=VR.dtype)
+    for r in range(VR.shape[1]):
+        x = VR[:, r:r + 1]
+        num = _seq_sum_cols(np.where(x < VC, x, VC), n_pf)
+        d = sr[r] + sc
+        with np.errstate(divide="ignore", invalid="ignore"):
+            v = (dt(2) * num) / d
+        out[r] = np.where(d == 0, dt(0), v)
+    return out
+
+
 def uniform_cols(seed: int, n_f: int, n_v: int, cols, dtype=np.float64):
     """Selected global columns of the uniform matrix."""
     q = np.arange(n_f, dtype=np.uint64)[:, None]

@@ -86,6 +86,8 @@ SIGNATURES = {
     "psim_czek2_streamed": (C.c_int, [C.c_int, C.POINTER(Block2), c_vp, c_i64, c_i64, c_vp,
                                       c_vp, c_vp]),
     "psim_stream_stats": (C.c_int, [C.POINTER(C.c_uint64), C.c_int]),
+    "psim_stream_error": (C.c_int, [C.POINTER(C.c_uint)]),
+    "psim_launch_count": (C.c_int, [C.POINTER(C.c_uint64), C.c_int]),
     "psim_quantize_bytes": (C.c_int, [C.c_int, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "psim_box3_plan": (C.c_int, [C.c_int, C.POINTER(Box3), C.POINTER(c_i64), C.POINTER(c_i64)]),
     "psim_mgemm_bits": (C.c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64,
@@ -152,3 +154,10 @@ def tile_shape(code: int) -> tuple[int, int]:
         call("psim_tile_shape", code, C.byref(r), C.byref(c))
         _shapes[code] = (r.value, c.value)
     return _shapes[code]
+
+
+def launch_count(reset: bool = False) -> int:
+    """Kernel launches libpsim issued in this process (psim_launch_count)."""
+    n = C.c_uint64(0)
+    call("psim_launch_count", C.byref(n), 1 if reset else 0)
+    return n.value

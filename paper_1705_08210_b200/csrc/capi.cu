@@ -1,6 +1,7 @@
 // extern "C" boundary of libpsim (declared in include/psim.h): argument
 // validation, error-status mapping and the host-side planning of 3-way
 // boxes. No kernel code lives here.
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -8,6 +9,14 @@
 
 #include "box3_plan.cuh"
 #include "psim_internal.h"
+
+namespace psim {
+
+static std::atomic<unsigned long long> g_launches{0};
+
+void note_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
+
+}  // namespace psim
 
 namespace {
 
@@ -281,6 +290,17 @@ int psim_czek2_streamed(int dtype, const psim_block2_t* t, const void* host, int
 int psim_stream_stats(unsigned long long* out4, int reset) {
   if (!out4) return fail(PSIM_ECONFIG, "NULL argument");
   return cuda_status(psim::stream_stats(out4, reset), "psim_stream_stats");
+}
+
+int psim_launch_count(unsigned long long* out, int reset) {
+  if (!out) return fail(PSIM_ECONFIG, "NULL argument");
+  *out = reset ? psim::g_launches.exchange(0) : psim::g_launches.load();
+  return PSIM_OK;
+}
+
+int psim_stream_error(unsigned* aborted) {
+  if (!aborted) return fail(PSIM_ECONFIG, "NULL argument");
+  return cuda_status(psim::stream_error(aborted, 0), "psim_stream_error");
 }
 
 int psim_czek2_from_numerators(int dtype, const void* N, int64_t r0, int64_t r1, int64_t m,

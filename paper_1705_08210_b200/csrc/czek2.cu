@@ -79,13 +79,19 @@ __device__ __forceinline__ int seg_of(const Args2<T>& a, int64_t c) {
 
 // kCzek2Streamed: the host uploads the block in chunks from the LAST vector
 // down (copy engine, flag after each chunk), so a tile whose lowest vector is
-// v may start once chunk(v)'s flag is set. Bounded spin: a flag that never
-// arrives traps (a kernel error) instead of hanging the GPU.
+// v may start once chunk(v)'s flag is set. Bounded spin: a flag that has not
+// arrived after kWaitLimitNs sets g_stream_abort and the CTA gives up (its
+// tile result is discarded); every other waiter sees the abort flag and
+// gives up at once, and the host turns the flag into EngineError
+// (psim_stream_error). No __trap(): the CUDA context, torch's and NCCL's
+// state survive a stalled upload.
 // Wait statistics of streamed runs (psim_stream_stats): total ns spent
 // waiting for input chunks / for column sums, count of sum waits, max wait.
 __device__ unsigned long long g_stream_wait[4];
+__device__ unsigned g_stream_abort;
+constexpr uint64_t kWaitLimitNs = 20000000000ull;  // 20 s
 
-__device__ __forceinline__ void wait_ready(const unsigned* flag, int kind) {
+__device__ __forceinline__ bool wait_ready(const unsigned* flag, int kind) {
   uint64_t t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   for (uint64_t t = t0;;) {
@@ -97,12 +103,35 @@ __device__ __forceinline__ void wait_ready(const unsigned* flag, int kind) {
         if (kind == 1) atomicAdd(&g_stream_wait[2], 1ull);
         atomicMax(&g_stream_wait[3], (unsigned long long)(t - t0));
       }
-      return;
+      return true;
     }
+    if (*(volatile unsigned*)&g_stream_abort) return false;
     __nanosleep(512);
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (t - t0 > 20000000000ull) __trap();  // 20 s
+    if (t - t0 > kWaitLimitNs) {
+      atomicExch(&g_stream_abort, 1u);
+      return false;
+    }
   }
+}
+
+// One thread waits; the CTA learns the outcome through shared memory.
+__device__ __forceinline__ bool cta_wait_ready(const unsigned* flag, int kind) {
+  __shared__ int ok;
+  if (threadIdx.x == 0) ok = wait_ready(flag, kind);
+  __syncthreads();
+  const bool r = ok;
+  __syncthreads();
+  return r;
+}
+
+cudaError_t stream_error(unsigned* aborted, int reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(aborted, g_stream_abort, sizeof(unsigned));
+  if (e == cudaSuccess && reset) {
+    const unsigned z = 0;
+    e = cudaMemcpyToSymbol(g_stream_abort, &z, sizeof(z));
+  }
+  return e;
 }
 
 cudaError_t stream_stats(unsigned long long* out4, int reset) {
@@ -148,8 +177,7 @@ __device__ void streamed_row_sums(const Args2<typename C::T>& a, int64_t r,
   using T = typename C::T;
   const int64_t v0 = r * C::BM;
   const int nv = (int)min64(C::BM, a.n - v0);
-  if (threadIdx.x == 0) wait_ready(a.ready + v0 / a.chunk, 0);
-  __syncthreads();
+  if (!cta_wait_ready(a.ready + v0 / a.chunk, 0)) return;  // aborted: sums never published
   T (*tile)[33] = reinterpret_cast<T (*)[33]>(smem);  // [BM][33]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   T acc = T(0);
@@ -196,6 +224,9 @@ __global__ void __launch_bounds__(kNT, C::MINB) k_minplus2(const Args2<typename 
     tb = streamed_tile(a);
     if (tb < 0) {
       streamed_row_sums<C>(a, -1 - tb, smem);
+      // keep the PDL invariant of every exit path (see the end of the kernel),
+      // although a streamed launch is never programmatically dependent
+      asm volatile("griddepcontrol.wait;" ::: "memory");
       return;
     }
   }
@@ -209,8 +240,7 @@ __global__ void __launch_bounds__(kNT, C::MINB) k_minplus2(const Args2<typename 
   {
     const int64_t row0 = (int64_t)bi * C::BM, col0 = (int64_t)bj * C::BN;
     if (STREAMED) {
-      if (threadIdx.x == 0) wait_ready(a.ready + min64(row0, col0) / a.chunk, 0);
-      __syncthreads();
+      if (!cta_wait_ready(a.ready + min64(row0, col0) / a.chunk, 0)) return;
     }
     if constexpr (MODE == kCzek2Flat) {
       // columns [col0, split) from segment s, the rest from segment s + 1
@@ -237,12 +267,15 @@ __global__ void __launch_bounds__(kNT, C::MINB) k_minplus2(const Args2<typename 
   if (STREAMED) {
     // the sums of this tile's rows and columns: published by the owners of
     // row tiles bi .. (col0 + cols - 1) / BM (columns lie at or right of the rows)
+    __shared__ int sums_ok;
     if (threadIdx.x == 0) {
-      wait_ready(a.sum_ready + bi, 1);
-      for (int64_t r = col0 / C::BM; r <= (col0 + cols - 1) / C::BM; ++r)
-        if (r != bi) wait_ready(a.sum_ready + r, 1);
+      bool ok = wait_ready(a.sum_ready + bi, 1);
+      for (int64_t r = col0 / C::BM; ok && r <= (col0 + cols - 1) / C::BM; ++r)
+        if (r != bi) ok = wait_ready(a.sum_ready + r, 1);
+      sums_ok = ok;
     }
     __syncthreads();
+    if (!sums_ok) return;
   }
   const int ty = thread_ty(), tx = thread_tx();
   if constexpr (MODE == kCzek2Flat) {
@@ -432,6 +465,7 @@ static cudaError_t launch_group(Args2<typename C::T>* args, const int64_t* row_b
     a.row_pref = pref + off;
     off += a.nbands + 1;
     const int64_t bm = is_edge(k) ? CE::BM : C::BM, bn = is_edge(k) ? CE::BN : C::BN;
+    note_launch();
     k_band_prefix<<<1, 1024, 0, st>>>(a.nbands, a.band, a.row_tile0, a.tiles_m, a.tiles_n, bm,
                                       bn, a.diagonal, pref + (a.row_pref - pref));
     e = cudaGetLastError();
@@ -450,6 +484,7 @@ static cudaError_t launch_group(Args2<typename C::T>* args, const int64_t* row_b
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const bool flat = args[k].nseg > 0;
+    note_launch();
     if (is_edge(k))
       e = flat ? cudaLaunchKernelEx(&cfg, k_minplus2<CE, FLAT_MODE>, args[k])
                : cudaLaunchKernelEx(&cfg, k_minplus2<CE, MODE>, args[k]);
@@ -642,6 +677,9 @@ cudaError_t czek2_streamed_t(const Czek2Block& t, const void* host, int64_t host
   if (e == cudaSuccess) e = cudaStreamWaitEvent(compute, cleared, 0);
   cudaEventDestroy(cleared);
   if (e != cudaSuccess) return e;
+  void* abort_flag = nullptr;  // cleared before every streamed launch
+  if ((e = cudaGetSymbolAddress(&abort_flag, g_stream_abort)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(abort_flag, 0, sizeof(unsigned), compute)) != cudaSuccess) return e;
   Args2<T> a = make_args<T>(t.W, t.ldw, t.V, t.ldv, t.n_f, t.m, t.n, 1);
   a.g_row = t.g_row;
   a.g_col = t.g_col;
@@ -735,6 +773,7 @@ cudaError_t czek2_from_num_t(const void* N, int64_t r0, int64_t r1, int64_t m, i
                              unsigned long long* acc, cudaStream_t st) {
   if (r1 <= r0) return cudaSuccess;
   if (r1 - r0 > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  note_launch();
   k_czek2_from_num<T><<<(unsigned)(r1 - r0), 256, 0, st>>>(
       static_cast<const T*>(N), r0, m, n, diagonal, static_cast<const T*>(s_row),
       static_cast<const T*>(s_col), g_row, g_col, n_v, static_cast<T*>(vals), acc);

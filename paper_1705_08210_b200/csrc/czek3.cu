@@ -312,11 +312,16 @@ static cudaError_t czek3_t(const Czek3Box& b, int64_t* work, int64_t n_single, i
   int64_t* tp = work;
   int64_t* op = work + nJ + 1;
   int64_t* pp = work + 2 * (nJ + 1);
+  note_launch();
   k_box3_prefix<<<1, 1024, 0, st>>>(b.i0, b.i1, b.j0, b.j1, b.k0, b.k1, C::BM, C::BN, work);
-  if (n_single > 0)
+  if (n_single > 0) {
+    note_launch();
     k_czek3<C, RAW, false><<<(unsigned)n_single, kNT, C::SMEM_BYTES, st>>>(b, tp, op, nJ);
-  if (n_packed > 0)
+  }
+  if (n_packed > 0) {
+    note_launch();
     k_czek3<C, RAW, true><<<(unsigned)n_packed, kNT, C::SMEM_BYTES, st>>>(b, pp, op, nJ);
+  }
   return cudaGetLastError();
 }
 
@@ -327,9 +332,11 @@ static cudaError_t czek3_from_num_t(const Czek3Box& b, int64_t* work, const void
   if (e1 <= e0) return cudaSuccess;
   const int64_t nJ = b.j1 - b.j0;
   int64_t* op = work + nJ + 1;
+  note_launch();
   k_box3_prefix<<<1, 1024, 0, st>>>(b.i0, b.i1, b.j0, b.j1, b.k0, b.k1, C::BM, C::BN, work);
   int64_t blocks = (e1 - e0 + 255) / 256;
   if (blocks > 148 * 32) blocks = 148 * 32;
+  note_launch();
   k_czek3_from_num<T><<<(unsigned)blocks, 256, 0, st>>>(b, op, nJ, static_cast<const T*>(n3), e0,
                                                         e1, static_cast<T*>(vals));
   return cudaGetLastError();

@@ -46,6 +46,7 @@ template <typename T, int KIND>
 static cudaError_t gen_t(uint64_t seed, uint64_t mask, int64_t n_v_total, int64_t f0, int64_t v0,
                          int64_t n_fp, int64_t n_vp, void* out, int64_t ld, cudaStream_t st) {
   if (n_fp <= 0 || n_vp <= 0) return cudaSuccess;
+  note_launch();
   k_gen<T, KIND><<<grid_for(n_fp * n_vp, 256), 256, 0, st>>>(seed, mask, n_v_total, f0, v0, n_fp,
                                                              n_vp, static_cast<T*>(out), ld);
   return cudaGetLastError();
@@ -100,10 +101,13 @@ cudaError_t check_block(int dtype, const void* V, int64_t n_fp, int64_t n_vp, in
                         unsigned long long* flags, cudaStream_t st) {
   if (n_fp <= 0 || n_vp <= 0) return cudaSuccess;
   const unsigned g = grid_for(n_fp * n_vp, 256);
-  if (dtype == kF64)
+  if (dtype == kF64) {
+    note_launch();
     k_check<double><<<g, 256, 0, st>>>(static_cast<const double*>(V), n_fp, n_vp, ld, flags);
-  else
+  } else {
+    note_launch();
     k_check<float><<<g, 256, 0, st>>>(static_cast<const float*>(V), n_fp, n_vp, ld, flags);
+  }
   return cudaGetLastError();
 }
 
@@ -139,12 +143,15 @@ cudaError_t column_sums(int dtype, const void* V, int64_t n_fp, int64_t n_vp, in
                         void* out, cudaStream_t st) {
   if (n_vp <= 0) return cudaSuccess;
   const unsigned g = (unsigned)((n_vp + 31) / 32);
-  if (dtype == kF64)
+  if (dtype == kF64) {
+    note_launch();
     k_colsum<double><<<g, 256, 0, st>>>(static_cast<const double*>(V), n_fp, n_vp, ld,
                                         static_cast<double*>(out));
-  else
+  } else {
+    note_launch();
     k_colsum<float><<<g, 256, 0, st>>>(static_cast<const float*>(V), n_fp, n_vp, ld,
                                        static_cast<float*>(out));
+  }
   return cudaGetLastError();
 }
 
@@ -158,12 +165,15 @@ __global__ void k_fold(T* __restrict__ dst, const T* __restrict__ src, int64_t c
 cudaError_t fold_add(int dtype, void* dst, const void* src, int64_t count, cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
   const unsigned g = grid_for(count, 256);
-  if (dtype == kF64)
+  if (dtype == kF64) {
+    note_launch();
     k_fold<double><<<g, 256, 0, st>>>(static_cast<double*>(dst), static_cast<const double*>(src),
                                       count);
-  else
+  } else {
+    note_launch();
     k_fold<float><<<g, 256, 0, st>>>(static_cast<float*>(dst), static_cast<const float*>(src),
                                      count);
+  }
   return cudaGetLastError();
 }
 
@@ -185,14 +195,17 @@ cudaError_t min_columns(int dtype, const void* V, int64_t n_fp, int64_t n_vp, in
                         const void* vj, void* out, int64_t ldo, cudaStream_t st) {
   if (n_fp <= 0 || n_vp <= 0) return cudaSuccess;
   const unsigned g = grid_for(n_fp * n_vp, 256);
-  if (dtype == kF64)
+  if (dtype == kF64) {
+    note_launch();
     k_min_columns<double><<<g, 256, 0, st>>>(static_cast<const double*>(V), n_fp, n_vp, ld,
                                              static_cast<const double*>(vj),
                                              static_cast<double*>(out), ldo);
-  else
+  } else {
+    note_launch();
     k_min_columns<float><<<g, 256, 0, st>>>(static_cast<const float*>(V), n_fp, n_vp, ld,
                                             static_cast<const float*>(vj),
                                             static_cast<float*>(out), ldo);
+  }
   return cudaGetLastError();
 }
 
@@ -255,12 +268,15 @@ cudaError_t quantize_bytes(int dtype, const void* vals, int64_t count, void* out
   const uintptr_t a = reinterpret_cast<uintptr_t>(vals), b = reinterpret_cast<uintptr_t>(out);
   const int vec = (a % 16 == 0) && (b % 8 == 0);
   auto* f = static_cast<unsigned long long*>(flag);
-  if (dtype == kF64)
+  if (dtype == kF64) {
+    note_launch();
     k_quantize<double><<<g, 256, 0, st>>>(static_cast<const double*>(vals), count,
                                           static_cast<uint8_t*>(out), f, vec);
-  else
+  } else {
+    note_launch();
     k_quantize<float><<<g, 256, 0, st>>>(static_cast<const float*>(vals), count,
                                          static_cast<uint8_t*>(out), f, vec);
+  }
   return cudaGetLastError();
 }
 

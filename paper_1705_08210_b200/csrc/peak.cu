@@ -81,8 +81,10 @@ static cudaError_t peak_t(int64_t iters, double* cmp_per_s, double* cmp_per_clk_
   cudaEvent_t ev0, ev1;
   cudaEventCreate(&ev0);
   cudaEventCreate(&ev1);
+  note_launch();
   k_peak<T, VAR><<<blocks, 256, 0, st>>>(iters / 10 + 1, T(1e-3), sink, cyc);  // warm-up
   cudaEventRecord(ev0, st);
+  note_launch();
   k_peak<T, VAR><<<blocks, 256, 0, st>>>(iters, T(1e-3), sink, cyc);
   cudaEventRecord(ev1, st);
   e = cudaEventSynchronize(ev1);

@@ -9,6 +9,10 @@
 
 namespace psim {
 
+// Process-wide count of kernel launches issued by libpsim (psim_launch_count):
+// every launch site calls note_launch() right before it launches.
+void note_launch(int n = 1);
+
 constexpr int kF32 = 0;
 constexpr int kF64 = 1;
 
@@ -40,6 +44,7 @@ cudaError_t czek2_streamed(int dtype, const Czek2Block& t, const void* host, int
                            int64_t chunk, unsigned* ready, cudaStream_t compute,
                            cudaStream_t copy);
 cudaError_t stream_stats(unsigned long long* out4, int reset);
+cudaError_t stream_error(unsigned* aborted, int reset);
 constexpr int64_t kStreamMaxFlags = 65536;  // data + sum flags of a streamed run
 // Sorenson (0/1) path: bit packing and the AND+POPC 2-way task (sorenson.cu).
 cudaError_t pack_bits(int dtype, const void* V, int64_t n_fp, int64_t n_vp, int64_t ld,

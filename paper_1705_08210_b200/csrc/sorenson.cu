@@ -113,12 +113,15 @@ cudaError_t pack_bits(int dtype, const void* V, int64_t n_fp, int64_t n_vp, int6
   int64_t warps = ((n_fp + 31) / 32) * n_vp;
   int64_t blocks = (warps + 7) / 8;
   if (blocks > 148 * 32) blocks = 148 * 32;
-  if (dtype == kF64)
+  if (dtype == kF64) {
+    note_launch();
     k_pack_bits<double><<<(unsigned)blocks, 256, 0, st>>>(static_cast<const double*>(V), n_fp,
                                                           n_vp, ld, words, ldw, flags);
-  else
+  } else {
+    note_launch();
     k_pack_bits<float><<<(unsigned)blocks, 256, 0, st>>>(static_cast<const float*>(V), n_fp,
                                                          n_vp, ld, words, ldw, flags);
+  }
   return cudaGetLastError();
 }
 
@@ -177,8 +180,10 @@ static cudaError_t sorenson_t(const psim_block2_t& t, cudaStream_t st) {
   int64_t* pref = nullptr;
   e = cudaMallocAsync(&pref, (a.nbands + 1) * sizeof(int64_t), st);
   if (e != cudaSuccess) return e;
+  note_launch();
   k_band_prefix_s<<<1, 32, 0, st>>>(a.nbands, a.band, a.tiles_m, a.tiles_n, a.diagonal, pref);
   a.row_pref = pref;
+  note_launch();
   k_sorenson2<VT><<<(unsigned)blocks, kNT, C::SMEM_BYTES, st>>>(a);
   e = cudaGetLastError();
   cudaError_t e2 = cudaFreeAsync(pref, st);
@@ -224,6 +229,7 @@ cudaError_t mgemm_bits(const uint32_t* W, int64_t ldw, const uint32_t* V, int64_
   cudaError_t e = cudaFuncSetAttribute(k_mgemm_bits, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        C::SMEM_BYTES);
   if (e != cudaSuccess) return e;
+  note_launch();
   k_mgemm_bits<<<(unsigned)blocks, kNT, C::SMEM_BYTES, st>>>(W, ldw, V, ldv, (n_rows + 31) / 32,
                                                              m, n, tiles_n, M, ldm);
   return cudaGetLastError();

@@ -165,6 +165,22 @@ def to_device(values, dtype, dev) -> torch.Tensor:
     return host.to(dev, non_blocking=True)
 
 
+def raise_on_stream_abort() -> None:
+    """EngineError when the last streamed kernel gave up waiting for an input
+    chunk (psim_stream_error; the kernel exits instead of trapping, so the
+    CUDA context stays usable)."""
+    import ctypes as C
+
+    from . import _native as N
+    from .domain import EngineError
+
+    flag = C.c_uint(0)
+    N.call("psim_stream_error", C.byref(flag))
+    if flag.value:
+        raise EngineError("streamed input did not arrive within 20 s (upload stalled); "
+                          "the run's results were discarded")
+
+
 def raise_on_flags(flags: torch.Tensor) -> None:
     bad, neg = (int(x) for x in to_host(flags))
     if bad:

@@ -197,20 +197,6 @@ def allgather_ops(me: int, n_pv: int, blocks: dict, sums: dict, peer) -> list:
 
 
 
-def _task_grids(tasks, bn: int) -> int:
-    """Grids psim_czek2_tasks launches for ``tasks`` (each with a band prefix):
-    consecutive full-row off-diagonal tasks >= bn wide are merged
-    (czek2.cu flatten_tasks), and a task whose rows end 1..96 past a multiple
-    of 128 adds a 32-row edge grid."""
-    groups = []
-    for t in tasks:
-        ok = not t.diagonal and t.r0 == 0 and t.c1 - t.c0 >= bn
-        if ok and groups and groups[-1][0] and groups[-1][1] == t.r1 and len(groups[-1][2]) < 16:
-            groups[-1][2].append(t)
-        else:
-            groups.append((ok, t.r1, [t]))
-    return sum(1 + int(0 < (r1 - g[0].r0) % 128 <= 96) for _, r1, g in groups)
-
 class Runner2:
     """One rank's 2-way pipeline over NCCL (also the multi-GPU bench harness)."""
 
@@ -234,19 +220,14 @@ class Runner2:
         tasks = [e for e in self.events if isinstance(e, Task2)]
         self.my_cmp = sum(problem.n_f // grid.n_pf * D.pair_count(t.r1 - t.r0, t.c1 - t.c0,
                                                                    t.diagonal) for t in tasks)
-        # our kernels per step: column sums (+ field fold), then the min-plus
-        # grids: fused mode one for the diagonal task and one for all others;
-        # a field split runs per task min-plus + (n_pf - 1) folds + epilogue
+        # min-plus grids per step (for the per-launch roofline figure): fused
+        # mode runs one group for the diagonal task and one for all others; a
+        # field split runs one per task. Launch totals come from libpsim's own
+        # counter (psim_launch_count), not from a model of its launch rules.
         if self.fused:
             grids = int(any(t.diagonal for t in tasks)) + int(any(not t.diagonal for t in tasks))
-            diag = [t for t in tasks if t.diagonal]
-            rest = [t for t in tasks if not t.diagonal]
-            bn = 128 if problem.precision == "double" else 64
-            self.launches_per_step = 1 + 2 * (_task_grids(diag, bn) + _task_grids(rest, bn))
         else:
             grids = len(tasks)
-            per_task = 1 if grid.n_pf == 1 else 1 + (grid.n_pf - 1) + 1
-            self.launches_per_step = 1 + (grid.n_pf - 1) + len(tasks) * per_task
         self.kernel_cmp_per_launch = self.my_cmp / max(1, grids)
 
     def peer(self, slab: int) -> int:
@@ -548,6 +529,7 @@ def run_2way_nccl(problem, grid, balance: str = "split", keep_values: bool = Tru
     if r.sink is not None:
         r.sink.finish()
     if r.flags is not None:  # streamed input, validated on the device: every rank raises
+        D.raise_on_stream_abort()
         dist.all_reduce(r.flags)
         D.raise_on_flags(r.flags)
     _mark("flags")

@@ -236,6 +236,7 @@ def run_streamed(problem, host: torch.Tensor, keep_values: bool, sink) -> Outcom
     _mark("checked")
     end.record()
     D.spin_event(end)
+    D.raise_on_stream_abort()
     lo, hi, deg = D.acc_words(acc)
     piece = PairPiece(0, 0, n, n, True, 0, n, vals)
     return Outcome([piece], lo, hi, deg, count, D.to_host(sums),
@@ -335,9 +336,6 @@ class Resident2:
         self.problem, self.grid = problem, grid
         self.code = D.code_of(problem.precision)
         n = problem.n_v
-        # column sums, then per task a band prefix + the fused min-plus grid:
-        # the 128-row task and, when n_v % 128 is 1..96, its 32-row edge task
-        self.launches_per_step = 1 + 2 * (1 + int(0 < n % 128 <= 96))
         self.kernel_cmp_per_launch = problem.n_f * (n * (n - 1) // 2)
 
     def setup(self) -> None:
@@ -355,7 +353,6 @@ class Resident2:
         sor = self.problem.metric == "sorenson"
         if sor:  # f3: pack 0/1 fields into words, then the AND+POPC kernel
             self.kernel_name = "k_sorenson2<T> (psim_sorenson2_block)"
-            self.launches_per_step = 4  # sums, pack, band prefix, kernel
             bits = D.pack_bits(b)
         if timed:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -264,8 +264,6 @@ class Runner3Dist:
         work = sum(box_count(b) for b in self.edge_boxes + self.rest_boxes)
         self.my_cmp = work * problem.n_f
         self.kernel_cmp_per_launch = self.my_cmp / max(1, nb)
-        # column sums, (prefix + box) per box, one min-plus per numerator table
-        self.launches_per_step = 1 + 2 * nb + grid.n_pv * (grid.n_pv + 1) // 2
 
     def peer(self, slab: int) -> int:
         from .domain import rank_of_coords
@@ -429,7 +427,6 @@ class Resident3:
         self.grid = DecompGrid()
         self.code = D.code_of(problem.precision)
         self.kernel_cmp_per_launch = None
-        self.launches_per_step = None
 
     def setup(self) -> None:
         dev = torch.device("cuda", torch.cuda.current_device())
@@ -447,8 +444,6 @@ class Resident3:
             sizes.append(sum(box_plan(box_struct(b, self.blocks, self.sums, self.tables, p.n_f,
                                                  p.n_v, None, self.acc))[0] for b in boxes))
         self.buf = torch.empty(max(sizes), dtype=D.torch_dtype(p.precision), device=dev)
-        launches = sum(len(b) for b in self.stage_boxes)
-        self.launches_per_step = 2 + 2 * launches  # sums, N2 table, (prefix, box) per box
         nb = sum(len(b) for b in self.stage_boxes)
         self.kernel_cmp_per_launch = p.n_f * (p.n_v * (p.n_v - 1) * (p.n_v - 2) // 6) / nb
 

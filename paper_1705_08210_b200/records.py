@@ -116,6 +116,10 @@ class LazyRecords(Sequence):
     def _build(self) -> None:
         if self._values is not None:
             return
+        if any(p.values is None for p in self._pieces):
+            raise ValueError("this run kept no metric values (keep_values=False): only "
+                             "len(records), the checksum and the degenerate count are "
+                             "available; run with keep_values=True to access records")
         if not self._pieces:
             self._index = np.zeros(0, np.int64)
             self._values = np.zeros(0, self._dtype)

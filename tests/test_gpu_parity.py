@@ -2,7 +2,9 @@
 runs and the CPU oracle. Bit-exact everywhere: the kernels keep the
 reference's per-element ascending-q summation order, so even general FP
 data matches bitwise."""
+import json
 import math
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -521,3 +523,56 @@ def test_flattened_offdiagonal_tasks_bitwise_vs_oracle(precision):
     res = P.run_2way(prob, P.DecompGrid(n_pv=5), host_values=True)
     assert (res.records.values.view(np.uint8) == want.view(np.uint8)).all()
     assert res.checksum.hex == cks
+
+
+CONFIG_CASES = json.loads((Path(__file__).resolve().parent / "golden" / "configs.json")
+                          .read_text())["cases"]
+
+
+@pytest.mark.parametrize("idx", range(len(CONFIG_CASES)),
+                         ids=[f"{c['config']}-{c['kind']}-pf{c['grid']['n_pf']}"
+                              f"pv{c['grid']['n_pv']}" for c in CONFIG_CASES])
+def test_config_shaped_golden(idx):
+    """The benchmarked configurations' shapes (n_f, dtype, bits and
+    decomposition of cfg2..cfg5, n_v reduced) against the reference's own
+    run_2way / run_3way (tests/golden/make_golden_configs.py): checksum,
+    record count, degenerate count and a spread of individual value bits,
+    all bitwise -- including the ascending-p_f fold of cfg5's field split
+    on general FP data."""
+    c = CONFIG_CASES[idx]
+    P = _api()
+    src = (P.gen_uniform(c["seed"], c["n_f"], c["n_v"]) if c["kind"] == "uniform"
+           else P.gen_random_exact(c["seed"], c["n_f"], c["n_v"], c["bits"]))
+    prob = P.Problem(c["arity"], c["n_f"], c["n_v"], src, c["precision"])
+    grid = P.DecompGrid(**c["grid"])
+    res = P.run_2way(prob, grid) if c["arity"] == 2 else P.run_3way(prob, grid)
+    assert res.checksum.hex == c["checksum"]
+    assert len(res.records) == c["records"]
+    assert res.degenerate_count == c["degenerate"]
+    from oracle import propsim_np as O
+
+    vals = res.records.values
+    for pos, bits in c["sample"].items():
+        assert format(int(O.value_bits(vals[int(pos):int(pos) + 1])[0]), "x") == bits, pos
+
+
+def test_full_cfg2_sampled_parity():
+    """cfg2 at full size (2-way FP64, 20000 x 40000, bits 20) through the
+    benchmark's own harness: >= 10^4 pairs (a grid of sampled rows x sampled
+    columns of the canonical triangle, plus its first / last rows and
+    columns) recomputed from their columns alone by the oracle, bitwise
+    (SURVEY 8d), and the checksum equals the checksum every N of the round-1
+    scaling runs produced."""
+    import bench
+    from paper_1705_08210_b200 import engine2
+
+    P = _api()
+    prob = P.Problem(2, 20000, 40000, P.gen_random_exact(2026, 20000, 40000, 20))
+    r = engine2.Resident2(prob, P.DecompGrid())
+    r.setup()
+    r.step()
+    par = bench.sampled_parity(r, prob, 20, 1, None)
+    assert par["sampled"] >= 10000, par
+    assert par["mismatches"] == 0, par
+    assert r.checksum_hex() == "73cac6d75612b5f4372130e4fd66716c"
+    r.teardown()

@@ -189,27 +189,3 @@ def test_checksum_host_utility_kat():
     assert P.checksum(recs, 3).hex == "edba53ceceb9a10ef2a32e809282cfdd"
     with pytest.raises(P.DataError):
         P.checksum(recs + recs[:1], 3)
-
-
-@pytest.mark.parametrize("n_pv", [2, 4, 5, 8])
-def test_fused_launch_count_follows_flattening(n_pv):
-    """dist._task_grids mirrors psim_czek2_tasks: consecutive full-row
-    off-diagonal tasks >= BN wide share one grid, split half-row tasks do not,
-    and a row count 1..96 past a multiple of 128 adds one 32-row edge grid."""
-    from paper_1705_08210_b200.dist import _task_grids
-
-    n_vp = 5000  # 39 * 128 + 8: every task has an edge grid
-    for p in range(n_pv):
-        tasks = [t for t in PL.plan_2way(P.DecompGrid(n_pv=n_pv), RankCoords(0, p, 0), n_vp, "split")
-                 if isinstance(t, PL.Task2)]
-        diag = [t for t in tasks if t.diagonal]
-        rest = [t for t in tasks if not t.diagonal]
-        assert _task_grids(diag, 128) == 2
-        half_rows = [t for t in rest if t.r1 - t.r0 < n_vp]
-        full_rows = [t for t in rest if t.r1 - t.r0 == n_vp]
-        # one merged full-row group (if any) + each half-row task, each with its edge grid
-        want = 2 * (int(bool(full_rows)) + len(half_rows))
-        assert _task_grids(rest, 128) == want, (p, [(t.r0, t.r1, t.c0, t.c1) for t in rest])
-    assert _task_grids([], 128) == 0
-    t = PL.Task2(0, 0, 0, 0, 128 + 100, 0, 128 + 100)  # 100 ragged rows: one 128-row tile
-    assert _task_grids([t], 128) == 1

@@ -81,6 +81,14 @@ def main():
         if g["n_pf"] * g["n_pv"] * g["n_pr"] != world or "stage" in c or c["kind"] == "matrix":
             continue
         cases.append((c, None))
+    # the benchmarked configurations' shapes (reduced n_v) run by the reference
+    # (tests/golden/configs.json): cfg2/cfg3 circulant, cfg4 tetrahedral, cfg5
+    # field split (its ordered fold on general FP data included)
+    conf = json.loads((ROOT / "tests" / "golden" / "configs.json").read_text())
+    for c in conf["cases"]:
+        g = c["grid"]
+        if g["n_pf"] * g["n_pv"] * g["n_pr"] == world:
+            cases.append((c, None))
     # extra grids checked against the local single-GPU run
     extra = [
         (2, "double", 1000, 240, dict(n_pv=world)),
