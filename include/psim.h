@@ -233,6 +233,119 @@ int psim_czek3_box_numerators(int dtype, const psim_box3_t* box, void* stream);
 int psim_czek3_from_numerators(int dtype, const psim_box3_t* box, const void* n3, int64_t e0,
                                int64_t e1, void* vals, void* stream);
 
+/* --- run-level runtime: the drop-in for run_2way / run_3way ---------------
+ * One process per GPU. A context holds the device, this process's rank in the
+ * job, the world size and (world > 1) an NCCL communicator plus a comm
+ * stream and a copy stream. psim_run2 / psim_run3 run this rank's whole part
+ * of a run -- the reference's rank_fn (metrics2.py:131-159,
+ * metrics3.py:82-113) and its transport calls (RankContext.send / receive /
+ * reduce_field_axis, engine.py:158-216) -- on the device: input block,
+ * column sums, the slab plan (circulant 2-way, schedule.py:116-142;
+ * tetrahedral 3-way, schedule.py:184-214), NCCL send/recv of blocks, the
+ * ordered field-axis fold as a grouped send/recv reduce-scatter, the fused
+ * kernels, and the _gather of metrics2.py:174-203 (checksum words, counts,
+ * degenerate count, traffic, elapsed: an NCCL all-gather). Synchronous:
+ * every rank returns once the global totals are known. Rank r has grid
+ * coordinates p_f = r % n_pf, p_v = (r / n_pf) % n_pv, p_r = r / (n_pf
+ * n_pv) (core.py:83-97); world must equal n_pf * n_pv * n_pr. */
+typedef struct psim_ctx psim_ctx;
+
+#define PSIM_NCCL_ID_BYTES 128
+
+/* input kinds of psim_problem_t (SyntheticSpec kinds, verify.py:126-147, or
+ * a caller block: this rank's (n_f / n_pf) x (n_v / n_pv) slab, vector i at
+ * block + i * ld elements, in device or host memory) */
+#define PSIM_INPUT_RANDOM_EXACT 0
+#define PSIM_INPUT_ANALYTIC 1
+#define PSIM_INPUT_UNIFORM 2
+#define PSIM_INPUT_DEVICE 3
+#define PSIM_INPUT_HOST 4
+
+/* psim_run flags */
+#define PSIM_RUN_BALANCE_REFERENCE 1 /* 2-way: the reference's unsplit half-offset block */
+#define PSIM_RUN_VALUES_SCRATCH 2    /* values stored to a reused workspace buffer (bench) */
+#define PSIM_RUN_NO_STREAM 4         /* pinned host input: plain upload, no streamed kernel */
+
+/* Problem (core.py:260-293). */
+typedef struct psim_problem {
+  int32_t arity; /* 2 or 3 */
+  int32_t dtype; /* PSIM_F32 / PSIM_F64 */
+  int64_t n_f, n_v;
+  int32_t input; /* PSIM_INPUT_* */
+  int32_t bits;  /* random-exact */
+  uint64_t seed; /* random-exact / uniform */
+  const void* block; /* PSIM_INPUT_DEVICE / _HOST */
+  int64_t ld;
+} psim_problem_t;
+
+/* DecompGrid (core.py:44-80). */
+typedef struct psim_grid {
+  int32_t n_pf, n_pv, n_pr, n_st;
+} psim_grid_t;
+
+/* One value piece of this rank, in canonical ids. kind 2 (PairPiece): v =
+ * {g_row, g_col, m, n, diagonal, r0, r1, 0}: rows [r0, r1) of the task's
+ * packed layout (psim_block2_t). kind 3 (BoxPiece): v = {i0, i1, j0, j1, k0,
+ * k1, e0, e1}: elements [e0, e1) of the box's pivot-major layout. */
+typedef struct psim_piece {
+  int64_t kind;
+  int64_t offset; /* first value in psim_out_t.vals */
+  int64_t count;
+  int64_t v[8];
+} psim_piece_t;
+
+/* Traffic (TrafficStats, engine.py:51-75): send-side messages / elements /
+ * bytes per reference phase (metrics2.py:34-39: 0 BLOCK, 1 BLOCK_K, 2 SUM,
+ * 3 SUM_K, 4 TASK, 5 PIPE). */
+#define PSIM_PHASES 6
+typedef struct psim_traffic {
+  int64_t messages[PSIM_PHASES], elements[PSIM_PHASES], nbytes[PSIM_PHASES];
+} psim_traffic_t;
+
+typedef struct psim_out {
+  /* caller-provided (may be NULL): */
+  void* vals;                  /* >= plan n_vals values (device or pinned host) */
+  psim_piece_t* pieces;        /* host, >= plan n_pieces entries */
+  void* sums;                  /* n_v global column sums (device or host) */
+  psim_traffic_t* rank_traffic; /* host, world entries (every rank's traffic) */
+  /* filled by the run: */
+  int64_t n_pieces, n_vals;  /* this rank */
+  uint64_t checksum[2];      /* global 128-bit checksum (lo, hi) */
+  int64_t count, degenerate; /* global */
+  int64_t local_count;       /* values this rank holds */
+  double elapsed;            /* device time of the run, max over ranks (s) */
+  psim_traffic_t traffic;    /* this rank */
+  double kernel_seconds;     /* this rank: CUDA-event time of its fused min-plus launches */
+  int64_t kernel_grids;      /* ... and how many launch groups (task groups / boxes) */
+} psim_out_t;
+
+typedef struct psim_plan {
+  int64_t n_pieces, n_vals, workspace_bytes;
+} psim_plan_t;
+
+/* 128-byte NCCL unique id (rank 0 creates it, every rank passes it on). */
+int psim_nccl_unique_id(uint8_t* id);
+/* Collective over all ranks when world > 1 (ncclCommInitRank). */
+int psim_ctx_create(int device, int rank, int world, const uint8_t* nccl_id, psim_ctx** ctx);
+int psim_ctx_destroy(psim_ctx* ctx);
+/* Sizes this rank's run needs (host-only): pieces, values, workspace bytes.
+ * stage: 3-way stage (-1: all stages), ignored for 2-way. */
+int psim_run_plan(const psim_ctx* ctx, const psim_problem_t* problem, const psim_grid_t* grid,
+                  int stage, int flags, psim_plan_t* plan);
+/* run_2way / run_3way for this rank (see above). workspace: device memory of
+ * at least plan.workspace_bytes (256-byte aligned). stream: the compute
+ * stream (the caller's order is respected). */
+int psim_run2(psim_ctx* ctx, const psim_problem_t* problem, const psim_grid_t* grid, int flags,
+              void* workspace, int64_t workspace_bytes, psim_out_t* out, void* stream);
+int psim_run3(psim_ctx* ctx, const psim_problem_t* problem, const psim_grid_t* grid, int stage,
+              int flags, void* workspace, int64_t workspace_bytes, psim_out_t* out, void* stream);
+/* checksum (verify.py:86-96) of `count` values with canonical indices
+ * idx[e] (idx == NULL: idx0 + e): acc[0..1] += sum mix64(t) * (mix64(bits)
+ * | 1) mod 2^128 (FP32 bits zero-extended, verify.py:58-65); acc[2] is not
+ * touched. vals / idx / acc on the device. */
+int psim_checksum(int dtype, const void* vals, const int64_t* idx, int64_t idx0, int64_t count,
+                  unsigned long long* acc, void* stream);
+
 /* --- measurement ----------------------------------------------------------- */
 /* Min+add issue-rate microbenchmark of the mainloop mix (roofline
  * denominator). Synchronous. */

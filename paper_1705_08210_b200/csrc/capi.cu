@@ -85,6 +85,17 @@ void box3_counts(int dtype, const psim_box3_t& b, std::vector<int64_t>* tile_pre
 
 }  // namespace
 
+namespace psim {
+// Error reporting for the other host translation units (runtime.cu).
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+}  // namespace psim
+
 extern "C" {
 
 int psim_version(void) { return PSIM_VERSION; }

@@ -280,4 +280,30 @@ cudaError_t quantize_bytes(int dtype, const void* vals, int64_t count, void* out
   return cudaGetLastError();
 }
 
+// checksum (verify.py:86-96) of a value array with canonical indices
+// idx[e] (or idx0 + e): grid-stride terms, CTA reduction, one 128-bit atomic
+// pair per CTA (psim_common.cuh).
+template <typename T>
+__global__ void __launch_bounds__(256) k_checksum(const T* __restrict__ vals,
+                                                  const int64_t* __restrict__ idx, int64_t idx0,
+                                                  int64_t count, unsigned long long* acc) {
+  Cks c;
+  for (int64_t e = blockIdx.x * 256ll + threadIdx.x; e < count; e += (int64_t)gridDim.x * 256)
+    c.term((uint64_t)(idx ? idx[e] : idx0 + e), Traits<T>::bits(vals[e]));
+  c.deg = 0;
+  cks_block_flush<256>(acc, c);
+}
+
+cudaError_t checksum(int dtype, const void* vals, const int64_t* idx, int64_t idx0, int64_t count,
+                     unsigned long long* acc, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  const unsigned g = grid_for(count, 256);
+  note_launch();
+  if (dtype == kF64)
+    k_checksum<double><<<g, 256, 0, st>>>(static_cast<const double*>(vals), idx, idx0, count, acc);
+  else
+    k_checksum<float><<<g, 256, 0, st>>>(static_cast<const float*>(vals), idx, idx0, count, acc);
+  return cudaGetLastError();
+}
+
 }  // namespace psim
