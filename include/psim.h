@@ -325,13 +325,18 @@ typedef struct psim_plan {
 
 /* 128-byte NCCL unique id (rank 0 creates it, every rank passes it on). */
 int psim_nccl_unique_id(uint8_t* id);
-/* Collective over all ranks when world > 1 (ncclCommInitRank). */
+/* Collective over all ranks when world > 1 (ncclCommInitRank). device -1
+ * makes a planning-only context (psim_run_plan works, no CUDA / NCCL). */
 int psim_ctx_create(int device, int rank, int world, const uint8_t* nccl_id, psim_ctx** ctx);
 int psim_ctx_destroy(psim_ctx* ctx);
 /* Sizes this rank's run needs (host-only): pieces, values, workspace bytes.
  * stage: 3-way stage (-1: all stages), ignored for 2-way. */
 int psim_run_plan(const psim_ctx* ctx, const psim_problem_t* problem, const psim_grid_t* grid,
                   int stage, int flags, psim_plan_t* plan);
+/* psim_run_plan plus this rank's value pieces (host-only; cap >= n_pieces):
+ * exactly the pieces psim_run2 / psim_run3 will report. */
+int psim_run_pieces(const psim_ctx* ctx, const psim_problem_t* problem, const psim_grid_t* grid,
+                    int stage, int flags, psim_plan_t* plan, psim_piece_t* pieces, int64_t cap);
 /* run_2way / run_3way for this rank (see above). workspace: device memory of
  * at least plan.workspace_bytes (256-byte aligned). stream: the compute
  * stream (the caller's order is respected). */

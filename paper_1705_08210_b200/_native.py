@@ -57,6 +57,62 @@ class Box3(C.Structure):
     ]
 
 
+class Problem(C.Structure):
+    """psim_problem_t"""
+
+    _fields_ = [
+        ("arity", C.c_int32), ("dtype", C.c_int32), ("n_f", c_i64), ("n_v", c_i64),
+        ("input", C.c_int32), ("bits", C.c_int32), ("seed", c_u64),
+        ("block", c_vp), ("ld", c_i64),
+    ]
+
+
+class Grid(C.Structure):
+    """psim_grid_t"""
+
+    _fields_ = [("n_pf", C.c_int32), ("n_pv", C.c_int32), ("n_pr", C.c_int32),
+                ("n_st", C.c_int32)]
+
+
+class Piece(C.Structure):
+    """psim_piece_t"""
+
+    _fields_ = [("kind", c_i64), ("offset", c_i64), ("count", c_i64), ("v", c_i64 * 8)]
+
+
+PHASES = 6
+
+
+class Traffic(C.Structure):
+    """psim_traffic_t"""
+
+    _fields_ = [("messages", c_i64 * PHASES), ("elements", c_i64 * PHASES),
+                ("nbytes", c_i64 * PHASES)]
+
+
+class Out(C.Structure):
+    """psim_out_t"""
+
+    _fields_ = [
+        ("vals", c_vp), ("pieces", C.POINTER(Piece)), ("sums", c_vp),
+        ("rank_traffic", C.POINTER(Traffic)),
+        ("n_pieces", c_i64), ("n_vals", c_i64), ("checksum", c_u64 * 2),
+        ("count", c_i64), ("degenerate", c_i64), ("local_count", c_i64),
+        ("elapsed", C.c_double), ("traffic", Traffic),
+        ("kernel_seconds", C.c_double), ("kernel_grids", c_i64),
+    ]
+
+
+class Plan(C.Structure):
+    """psim_plan_t"""
+
+    _fields_ = [("n_pieces", c_i64), ("n_vals", c_i64), ("workspace_bytes", c_i64)]
+
+
+INPUT_RANDOM_EXACT, INPUT_ANALYTIC, INPUT_UNIFORM, INPUT_DEVICE, INPUT_HOST = range(5)
+RUN_BALANCE_REFERENCE, RUN_VALUES_SCRATCH, RUN_NO_STREAM = 1, 2, 4
+
+
 # name -> (restype, argtypes); every symbol declared in include/psim.h
 SIGNATURES = {
     "psim_version": (C.c_int, []),
@@ -99,6 +155,18 @@ SIGNATURES = {
     "psim_czek3_box_numerators": (C.c_int, [C.c_int, C.POINTER(Box3), c_vp]),
     "psim_czek3_from_numerators": (
         C.c_int, [C.c_int, C.POINTER(Box3), c_vp, c_i64, c_i64, c_vp, c_vp]),
+    "psim_nccl_unique_id": (C.c_int, [c_vp]),
+    "psim_ctx_create": (C.c_int, [C.c_int, C.c_int, C.c_int, c_vp, C.POINTER(c_vp)]),
+    "psim_ctx_destroy": (C.c_int, [c_vp]),
+    "psim_run_plan": (C.c_int, [c_vp, C.POINTER(Problem), C.POINTER(Grid), C.c_int, C.c_int,
+                                C.POINTER(Plan)]),
+    "psim_run_pieces": (C.c_int, [c_vp, C.POINTER(Problem), C.POINTER(Grid), C.c_int, C.c_int,
+                                  C.POINTER(Plan), C.POINTER(Piece), c_i64]),
+    "psim_run2": (C.c_int, [c_vp, C.POINTER(Problem), C.POINTER(Grid), C.c_int, c_vp, c_i64,
+                            C.POINTER(Out), c_vp]),
+    "psim_run3": (C.c_int, [c_vp, C.POINTER(Problem), C.POINTER(Grid), C.c_int, C.c_int, c_vp,
+                            c_i64, C.POINTER(Out), c_vp]),
+    "psim_checksum": (C.c_int, [C.c_int, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp]),
     "psim_peak_minplus": (
         C.c_int, [C.c_int, C.c_int, c_i64, C.POINTER(C.c_double), C.POINTER(C.c_double), c_vp]),
 }

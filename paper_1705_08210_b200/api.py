@@ -129,9 +129,19 @@ def _result(problem, grid, transport, out, stages, kern: str = "b200") -> RunRes
     return RunResult(
         arity=problem.arity, n_f=problem.n_f, n_v=problem.n_v, precision=problem.precision,
         metric=problem.metric, grid=grid, transport=transport, kernel=kern, records=recs,
-        checksum=Checksum128.from_words(out.lo, out.hi), traffic=TrafficStats(),
-        rank_traffic={}, degenerate_count=out.degenerate, elapsed=out.elapsed, stages=stages,
+        checksum=Checksum128.from_words(out.lo, out.hi),
+        traffic=out.traffic if out.traffic is not None else TrafficStats(),
+        rank_traffic=dict(out.rank_traffic), degenerate_count=out.degenerate,
+        elapsed=out.elapsed, stages=stages,
     )
+
+
+def _nccl_runtime():
+    """transport="nccl": libpsim's run-level runtime (psim_run2 / psim_run3
+    drive the kernels and their own NCCL communicator, runtime.py)."""
+    from . import runtime
+
+    return runtime
 
 
 def run_2way(problem, grid, *, transport: str = "local", kernel: str | None = None,
@@ -152,12 +162,10 @@ def run_2way(problem, grid, *, transport: str = "local", kernel: str | None = No
     # (like the reference, only the bit-packed path checks for 0/1 input --
     # on the device, while packing: metrics2.py:125-136, mingemm.py:287-288)
     if mode == "nccl":
-        from . import dist
-
         if kern == "bitpacked":  # NCCL ranks run the dense kernel: bitwise identical on 0/1
             _check_sorenson(problem)
-        out = dist.run_2way_nccl(problem, grid, balance=balance, keep_values=keep_values,
-                                 host_values=host_values)
+        out = _nccl_runtime().run(problem, grid, None, keep_values=keep_values,
+                                  host_values=host_values, balance=balance)
     else:
         if kern == "bitpacked" and grid.n_pf > 1:
             _check_sorenson(problem)  # field split: dense kernel, identical bits on 0/1
@@ -186,9 +194,8 @@ def run_3way(problem, grid, *, stage: int | None = None, transport: str = "local
     _check_sorenson(problem)  # 3-way always checks (metrics3.py:84-85); dense kernel
     _require_cuda()
     if mode == "nccl":
-        from . import dist
-
-        out = dist.run_3way_nccl(problem, grid, stages, keep_values=keep_values)
+        out = _nccl_runtime().run(problem, grid, stage, keep_values=keep_values,
+                                  host_values=host_values)
     else:
         out = engine3.run_local(problem, grid, stages, keep_values=keep_values,
                                 host_values=host_values)

@@ -1068,7 +1068,8 @@ struct Run3 : Rank {
 
 template <class R>
 int plan_or_run(psim_ctx* ctx, const psim_problem_t* p, const psim_grid_t* g, int stage, int flags,
-                void* ws, int64_t ws_bytes, psim_out_t* out, void* stream, psim_plan_t* plan) {
+                void* ws, int64_t ws_bytes, psim_out_t* out, void* stream, psim_plan_t* plan,
+                psim_piece_t* plan_pieces = nullptr, int64_t cap = 0) {
   R r;
   r.ctx = ctx;
   r.pr = p;
@@ -1083,6 +1084,12 @@ int plan_or_run(psim_ctx* ctx, const psim_problem_t* p, const psim_grid_t* g, in
     plan->n_pieces = (int64_t)r.pieces.size();
     plan->n_vals = r.n_vals;
     plan->workspace_bytes = r.A.off + 256;
+    if (plan_pieces) {
+      if (cap < plan->n_pieces)
+        return set_error(PSIM_ECONFIG, "pieces capacity %lld < %lld", (long long)cap,
+                         (long long)plan->n_pieces);
+      std::copy(r.pieces.begin(), r.pieces.end(), plan_pieces);
+    }
     return PSIM_OK;
   }
   if (r.A.off + 256 > ws_bytes || (!ws && r.A.off > 0))
@@ -1126,6 +1133,14 @@ int psim_ctx_create(int device, int rank, int world, const uint8_t* nccl_id, psi
   *out = nullptr;
   if (world < 1 || rank < 0 || rank >= world)
     return set_error(PSIM_ECONFIG, "rank %d outside world %d", rank, world);
+  if (device < 0) {  // planning-only context (psim_run_plan; no CUDA, no NCCL)
+    psim_ctx* c = new psim_ctx;
+    c->device = -1;
+    c->rank = rank;
+    c->world = world;
+    *out = c;
+    return PSIM_OK;
+  }
   if (world > 1 && !nccl_id) return set_error(PSIM_ECONFIG, "world > 1 needs an NCCL unique id");
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess)
@@ -1169,20 +1184,28 @@ int psim_ctx_destroy(psim_ctx* c) {
 
 int psim_run_plan(const psim_ctx* ctx, const psim_problem_t* p, const psim_grid_t* g, int stage,
                   int flags, psim_plan_t* plan) {
+  return psim_run_pieces(ctx, p, g, stage, flags, plan, nullptr, 0);
+}
+
+int psim_run_pieces(const psim_ctx* ctx, const psim_problem_t* p, const psim_grid_t* g, int stage,
+                    int flags, psim_plan_t* plan, psim_piece_t* pieces, int64_t cap) {
   if (!plan) return set_error(PSIM_ECONFIG, "NULL plan");
   if (int r = check_common(ctx, p, g, p ? p->arity : 0)) return r;
   if (p->arity != 2 && p->arity != 3) return set_error(PSIM_ECONFIG, "arity must be 2 or 3");
   if (p->arity == 3 && (stage < -1 || stage >= g->n_st))
     return set_error(PSIM_ECONFIG, "stage %d outside [0, %d)", stage, g->n_st);
   psim_ctx* c = const_cast<psim_ctx*>(ctx);
-  return p->arity == 2 ? plan_or_run<Run2>(c, p, g, -1, flags, nullptr, 0, nullptr, nullptr, plan)
-                       : plan_or_run<Run3>(c, p, g, stage, flags, nullptr, 0, nullptr, nullptr, plan);
+  return p->arity == 2
+             ? plan_or_run<Run2>(c, p, g, -1, flags, nullptr, 0, nullptr, nullptr, plan, pieces, cap)
+             : plan_or_run<Run3>(c, p, g, stage, flags, nullptr, 0, nullptr, nullptr, plan, pieces,
+                                 cap);
 }
 
 int psim_run2(psim_ctx* ctx, const psim_problem_t* p, const psim_grid_t* g, int flags, void* ws,
               int64_t ws_bytes, psim_out_t* out, void* stream) {
   if (int r = check_common(ctx, p, g, 2)) return r;
   if (!out) return set_error(PSIM_ECONFIG, "NULL out");
+  if (ctx->device < 0) return set_error(PSIM_ECONFIG, "planning-only context (device -1)");
   if (ctx->world > 1 && nccl().error) return set_error(PSIM_ERUNTIME, "%s", nccl().error);
   cudaSetDevice(ctx->device);
   return plan_or_run<Run2>(ctx, p, g, -1, flags, ws, ws_bytes, out, stream, nullptr);
@@ -1192,6 +1215,7 @@ int psim_run3(psim_ctx* ctx, const psim_problem_t* p, const psim_grid_t* g, int 
               void* ws, int64_t ws_bytes, psim_out_t* out, void* stream) {
   if (int r = check_common(ctx, p, g, 3)) return r;
   if (!out) return set_error(PSIM_ECONFIG, "NULL out");
+  if (ctx->device < 0) return set_error(PSIM_ECONFIG, "planning-only context (device -1)");
   if (stage < -1 || stage >= g->n_st)
     return set_error(PSIM_ECONFIG, "stage %d outside [0, %d)", stage, g->n_st);
   if (ctx->world > 1 && nccl().error) return set_error(PSIM_ERUNTIME, "%s", nccl().error);

@@ -37,8 +37,9 @@ class Outcome:
     count: int = 0
     sums: np.ndarray | None = None
     elapsed: float = 0.0
-    traffic: dict = field(default_factory=dict)
+    traffic: object = None  # TrafficStats of this process (nccl runtime), else None
     local_count: int | None = None  # records held by this process (nccl: its share)
+    rank_traffic: dict = field(default_factory=dict)  # rank -> TrafficStats
 
 
 def fold_sums(parts: list[torch.Tensor], code: int) -> torch.Tensor:
