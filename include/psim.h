@@ -323,6 +323,21 @@ typedef struct psim_plan {
   int64_t n_pieces, n_vals, workspace_bytes;
 } psim_plan_t;
 
+/* One point-to-point message of a run (psim_run_comms): in NCCL group
+ * `group` (groups are issued in ascending order), a send (op 0) to or a
+ * receive (op 1) from rank `peer` of `bytes` bytes carrying `what` (PSIM_MSG_*)
+ * for `slot`: the slab whose block / sums travel (BLOCK, SUMS), the task /
+ * table / box index (TASK, TABLE, BOX). */
+#define PSIM_MSG_BLOCK 0
+#define PSIM_MSG_SUMS 1
+#define PSIM_MSG_TASK 2
+#define PSIM_MSG_TABLE 3
+#define PSIM_MSG_BOX 4
+typedef struct psim_msg {
+  int32_t group, op, peer, what;
+  int64_t bytes, slot;
+} psim_msg_t;
+
 /* 128-byte NCCL unique id (rank 0 creates it, every rank passes it on). */
 int psim_nccl_unique_id(uint8_t* id);
 /* Collective over all ranks when world > 1 (ncclCommInitRank). device -1
@@ -337,6 +352,10 @@ int psim_run_plan(const psim_ctx* ctx, const psim_problem_t* problem, const psim
  * exactly the pieces psim_run2 / psim_run3 will report. */
 int psim_run_pieces(const psim_ctx* ctx, const psim_problem_t* problem, const psim_grid_t* grid,
                     int stage, int flags, psim_plan_t* plan, psim_piece_t* pieces, int64_t cap);
+/* The point-to-point messages this rank's psim_run2 / psim_run3 issues, in
+ * order (host-only, any context): *n = count; up to cap written to msgs. */
+int psim_run_comms(const psim_ctx* ctx, const psim_problem_t* problem, const psim_grid_t* grid,
+                   int stage, int flags, psim_msg_t* msgs, int64_t cap, int64_t* n);
 /* run_2way / run_3way for this rank (see above). workspace: device memory of
  * at least plan.workspace_bytes (256-byte aligned). stream: the compute
  * stream (the caller's order is respected). */
@@ -344,6 +363,12 @@ int psim_run2(psim_ctx* ctx, const psim_problem_t* problem, const psim_grid_t* g
               void* workspace, int64_t workspace_bytes, psim_out_t* out, void* stream);
 int psim_run3(psim_ctx* ctx, const psim_problem_t* problem, const psim_grid_t* grid, int stage,
               int flags, void* workspace, int64_t workspace_bytes, psim_out_t* out, void* stream);
+/* Memory helpers for callers without a CUDA allocator of their own (the
+ * reference-side ctypes binding): device (pinned_host = 0)
+ * or page-locked host memory; psim_memcpy is a synchronous cudaMemcpyDefault. */
+int psim_malloc(void** ptr, int64_t bytes, int pinned_host);
+int psim_free(void* ptr, int pinned_host);
+int psim_memcpy(void* dst, const void* src, int64_t bytes);
 /* checksum (verify.py:86-96) of `count` values with canonical indices
  * idx[e] (idx == NULL: idx0 + e): acc[0..1] += sum mix64(t) * (mix64(bits)
  * | 1) mod 2^128 (FP32 bits zero-extended, verify.py:58-65); acc[2] is not

@@ -103,6 +103,16 @@ class Out(C.Structure):
     ]
 
 
+class Msg(C.Structure):
+    """psim_msg_t"""
+
+    _fields_ = [("group", C.c_int32), ("op", C.c_int32), ("peer", C.c_int32),
+                ("what", C.c_int32), ("bytes", c_i64), ("slot", c_i64)]
+
+
+MSG_BLOCK, MSG_SUMS, MSG_TASK, MSG_TABLE, MSG_BOX = range(5)
+
+
 class Plan(C.Structure):
     """psim_plan_t"""
 
@@ -162,10 +172,15 @@ SIGNATURES = {
                                 C.POINTER(Plan)]),
     "psim_run_pieces": (C.c_int, [c_vp, C.POINTER(Problem), C.POINTER(Grid), C.c_int, C.c_int,
                                   C.POINTER(Plan), C.POINTER(Piece), c_i64]),
+    "psim_run_comms": (C.c_int, [c_vp, C.POINTER(Problem), C.POINTER(Grid), C.c_int, C.c_int,
+                                 C.POINTER(Msg), c_i64, C.POINTER(c_i64)]),
     "psim_run2": (C.c_int, [c_vp, C.POINTER(Problem), C.POINTER(Grid), C.c_int, c_vp, c_i64,
                             C.POINTER(Out), c_vp]),
     "psim_run3": (C.c_int, [c_vp, C.POINTER(Problem), C.POINTER(Grid), C.c_int, C.c_int, c_vp,
                             c_i64, C.POINTER(Out), c_vp]),
+    "psim_malloc": (C.c_int, [C.POINTER(c_vp), c_i64, C.c_int]),
+    "psim_free": (C.c_int, [c_vp, C.c_int]),
+    "psim_memcpy": (C.c_int, [c_vp, c_vp, c_i64]),
     "psim_checksum": (C.c_int, [C.c_int, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp]),
     "psim_peak_minplus": (
         C.c_int, [C.c_int, C.c_int, c_i64, C.POINTER(C.c_double), C.POINTER(C.c_double), c_vp]),

@@ -395,24 +395,72 @@ struct Rank {
     }
   }
 
+  // --- point-to-point plumbing -------------------------------------------
+  // Every NCCL send / recv of a run goes through send() / recv() inside a
+  // gstart() / gend() group, and is appended to `log` (psim_run_comms returns
+  // it; with `trace` set nothing is issued -- the CPU tests replay the log over
+  // gloo to check the schedule for every grid, N = 8 included).
+  std::vector<psim_msg_t> log;
+  int group = 0;
+  bool trace = false;
+
+  bool gstart() { return trace || S.nc(nccl().GroupStart(), "ncclGroupStart"); }
+  bool gend() {
+    ++group;
+    return trace || S.nc(nccl().GroupEnd(), "ncclGroupEnd");
+  }
+  bool send(const void* p, int64_t bytes, int peer, cudaStream_t s, int phase, int64_t elems,
+            int what, int64_t slot) {
+    log.push_back({group, 0, peer, what, bytes, slot});
+    count_send(phase, elems, bytes);
+    return trace || S.nc(nccl().Send(p, bytes, ncclChar, peer, ctx->comm, s), "ncclSend");
+  }
+  bool recv(void* p, int64_t bytes, int peer, cudaStream_t s, int what, int64_t slot) {
+    log.push_back({group, 1, peer, what, bytes, slot});
+    return trace || S.nc(nccl().Recv(p, bytes, ncclChar, peer, ctx->comm, s), "ncclRecv");
+  }
+
   // Grouped p2p all-gather of `bytes` from every field rank of this slab
   // (p_f order) into dst[n_pf][bytes]; dst[p_f] already holds ours.
-  bool field_allgather(const void* mine, void* dst, int64_t bytes, int phase, int64_t elems) {
-    const Nccl& N = nccl();
+  bool field_allgather(const void* mine, void* dst, int64_t bytes, int phase, int64_t elems,
+                       int what, int64_t slot) {
     char* d = static_cast<char*>(dst);
-    if (d + p_f * bytes != mine &&
+    if (!trace && d + p_f * bytes != mine &&
         !S.cuda(cudaMemcpyAsync(d + p_f * bytes, mine, bytes, cudaMemcpyDeviceToDevice, st),
                 "stage field part"))
       return false;
-    if (!S.nc(N.GroupStart(), "ncclGroupStart")) return false;
+    if (!gstart()) return false;
     for (int f = 0; f < g->n_pf; ++f) {
       if (f == p_f) continue;
       const int peer = rank_of(f, p_v, p_r);
-      S.nc(N.Send(mine, bytes, ncclChar, peer, ctx->comm, st), "ncclSend");
-      S.nc(N.Recv(d + f * bytes, bytes, ncclChar, peer, ctx->comm, st), "ncclRecv");
-      count_send(phase, elems, bytes);
+      send(mine, bytes, peer, st, phase, elems, what, slot);
+      recv(d + f * bytes, bytes, peer, st, what, slot);
     }
-    return S.nc(N.GroupEnd(), "ncclGroupEnd");
+    return gend();
+  }
+
+  // Ordered reduce-scatter over the field group (reduce_field_axis,
+  // engine.py:197-216): element range [off[f], off[f+1]) of `part` goes to
+  // field rank f; ours lands in rbuf[f][mine] from every f.
+  bool field_scatter(const void* part, void* rbuf_, const std::vector<int64_t>& off, int phase,
+                     int what, int64_t slot) {
+    const int64_t mine = off[p_f + 1] - off[p_f];
+    char* rb = static_cast<char*>(rbuf_);
+    const char* pp = static_cast<const char*>(part);
+    if (!gstart()) return false;
+    for (int f = 0; f < g->n_pf; ++f) {
+      const int64_t cnt = off[f + 1] - off[f];
+      if (f == p_f) {
+        if (!trace && cnt)
+          S.cuda(cudaMemcpyAsync(rb + f * mine * esz, pp + off[f] * esz, cnt * esz,
+                                 cudaMemcpyDeviceToDevice, st), "stage part");
+        continue;
+      }
+      const int peer = rank_of(f, p_v, p_r);
+      if (cnt) send(pp + off[f] * esz, cnt * esz, peer, st, phase, cnt, what, slot);
+      if (mine) recv(rb + f * mine * esz, mine * esz, peer, st, what, slot);
+    }
+    return gend();
   }
 
   // reduce_field_axis (engine.py:197-216): ((P0 + P1) + P2) + ... in p_f order.
@@ -429,7 +477,7 @@ struct Rank {
     if (!S.cuda(psim::column_sums(dtype, own, n_fp, n_vp, own_ld, s_own, st), "column sums"))
       return false;
     if (g->n_pf == 1) return true;
-    return field_allgather(s_own, sum_parts, n_vp * esz, 2, n_vp) &&
+    return field_allgather(s_own, sum_parts, n_vp * esz, 2, n_vp, PSIM_MSG_SUMS, p_v) &&
            fold_parts(s_own, sum_parts, n_vp);
   }
 
@@ -687,22 +735,38 @@ struct Run2 : Rank {
   // `ready` (the own block and its sums) has been reached on `after`.
   bool post_exchanges(cudaStream_t after) {
     if (ex.empty()) return true;
-    const Nccl& N = nccl();
-    if (!S.cuda(cudaEventRecord(ev_tmp, after), "event") ||
-        !S.cuda(cudaStreamWaitEvent(ctx->cstream, ev_tmp, 0), "wait"))
+    if (!trace && (!S.cuda(cudaEventRecord(ev_tmp, after), "event") ||
+                   !S.cuda(cudaStreamWaitEvent(ctx->cstream, ev_tmp, 0), "wait")))
       return false;
     for (size_t k = 0; k < ex.size(); ++k) {
       const int to = rank_of(p_f, ex[k].send_to, p_r), from = rank_of(p_f, ex[k].recv_from, p_r);
-      S.nc(N.GroupStart(), "ncclGroupStart");
-      S.nc(N.Send(own, n_vp * own_ld * esz, ncclChar, to, ctx->comm, ctx->cstream), "ncclSend");
-      S.nc(N.Send(s_own, n_vp * esz, ncclChar, to, ctx->comm, ctx->cstream), "ncclSend");
-      S.nc(N.Recv(rblock[k], n_vp * ld * esz, ncclChar, from, ctx->comm, ctx->cstream), "ncclRecv");
-      S.nc(N.Recv(rsums[k], n_vp * esz, ncclChar, from, ctx->comm, ctx->cstream), "ncclRecv");
-      if (!S.nc(N.GroupEnd(), "ncclGroupEnd")) return false;
-      count_send(0, n_fp * n_vp, n_fp * n_vp * esz);
-      count_send(2, n_vp, n_vp * esz);
+      cudaStream_t cs = ctx->cstream;
+      gstart();
+      send(own, n_vp * own_ld * esz, to, cs, 0, n_fp * n_vp, PSIM_MSG_BLOCK, p_v);
+      send(s_own, n_vp * esz, to, cs, 2, n_vp, PSIM_MSG_SUMS, p_v);
+      recv(rblock[k], n_vp * ld * esz, from, cs, PSIM_MSG_BLOCK, ex[k].recv_from);
+      recv(rsums[k], n_vp * esz, from, cs, PSIM_MSG_SUMS, ex[k].recv_from);
+      if (!gend()) return false;
     }
     return true;
+  }
+
+  // The comm schedule alone (psim_run_comms): execute()'s groups, in order.
+  void comm_trace() {
+    if (g->n_pf > 1) field_allgather(s_own, sum_parts, n_vp * esz, 2, n_vp, PSIM_MSG_SUMS, p_v);
+    post_exchanges(st);
+    if (g->n_pf > 1)
+      for (size_t k = 0; k < tasks.size(); ++k) field_scatter(part, rbuf, task_offsets(k), 4,
+                                                               PSIM_MSG_TASK, (int64_t)k);
+  }
+
+  std::vector<int64_t> task_offsets(size_t k) const {
+    const Task2& t = tasks[k];
+    const int64_t m = t.r1 - t.r0, n = t.c1 - t.c0;
+    const std::vector<int64_t> b = row_chunks(m, n, t.diag(), g->n_pf);
+    std::vector<int64_t> off(g->n_pf + 1);
+    for (int f = 0; f <= g->n_pf; ++f) off[f] = packed_offset(b[f], m, n, t.diag());
+    return off;
   }
 
   int slot_of(int step) const {
@@ -752,7 +816,6 @@ struct Run2 : Rank {
     if (!ex.empty() && (!S.cuda(cudaEventRecord(ev_tmp, ctx->cstream), "event") ||
                         !S.cuda(cudaStreamWaitEvent(st, ev_tmp, 0), "wait")))
       return false;
-    const Nccl& N = nccl();
     for (size_t k = 0; k < tasks.size(); ++k) {
       const Task2& t = tasks[k];
       const int64_t m = t.r1 - t.r0, n = t.c1 - t.c0;
@@ -771,27 +834,9 @@ struct Run2 : Rank {
           !S.psim(psim_mgemm(dtype, W, own_ld, Vc, ldv, n_fp, m, n, t.diag(), part, 0, 1, st)) ||
           !kmark())
         return false;
-      const std::vector<int64_t> b = row_chunks(m, n, t.diag(), g->n_pf);
-      std::vector<int64_t> off(g->n_pf + 1);
-      for (int f = 0; f <= g->n_pf; ++f) off[f] = packed_offset(b[f], m, n, t.diag());
+      const std::vector<int64_t> off = task_offsets(k);
       const int64_t mine = off[p_f + 1] - off[p_f];
-      char* rb = static_cast<char*>(rbuf);
-      S.nc(N.GroupStart(), "ncclGroupStart");
-      for (int f = 0; f < g->n_pf; ++f) {
-        const int64_t sz = (off[f + 1] - off[f]) * esz;
-        if (f == p_f) {
-          S.cuda(cudaMemcpyAsync(rb + f * mine * esz, static_cast<char*>(part) + off[f] * esz, sz,
-                                 cudaMemcpyDeviceToDevice, st), "stage part");
-          continue;
-        }
-        const int peer = rank_of(f, p_v, p_r);
-        if (sz) S.nc(N.Send(static_cast<char*>(part) + off[f] * esz, sz, ncclChar, peer, ctx->comm, st),
-                     "ncclSend");
-        if (mine) S.nc(N.Recv(rb + f * mine * esz, mine * esz, ncclChar, peer, ctx->comm, st),
-                       "ncclRecv");
-        if (sz) count_send(4, off[f + 1] - off[f], sz);
-      }
-      if (!S.nc(N.GroupEnd(), "ncclGroupEnd")) return false;
+      if (!field_scatter(part, rbuf, off, 4, PSIM_MSG_TASK, (int64_t)k)) return false;
       if (mine == 0) continue;
       if (!fold_parts(tot, rbuf, mine)) return false;
       const psim_piece_t& pc = pieces[k];
@@ -961,34 +1006,65 @@ struct Run3 : Rank {
     return true;
   }
 
+  bool blocks_group() {
+    if (g->n_pv == 1) return true;
+    cudaStream_t cs = ctx->cstream;
+    if (!gstart()) return false;
+    for (int d = 1; d < g->n_pv; ++d) {
+      const int to = rank_of(p_f, (p_v - d + g->n_pv) % g->n_pv, p_r);
+      const int fs = (p_v + d) % g->n_pv;
+      const int from = rank_of(p_f, fs, p_r);
+      send(own, n_vp * ld * esz, to, cs, 0, n_fp * n_vp, PSIM_MSG_BLOCK, p_v);
+      send(s_own, n_vp * esz, to, cs, 2, n_vp, PSIM_MSG_SUMS, p_v);
+      recv(blocks[fs], n_vp * ld * esz, from, cs, PSIM_MSG_BLOCK, fs);
+      recv(bsums[fs], n_vp * esz, from, cs, PSIM_MSG_SUMS, fs);
+    }
+    return gend();
+  }
+
+  bool table_group(size_t t, const void* mine) {
+    return field_allgather(mine, tab_parts, n_vp * n_vp * esz, 4, n_vp * n_vp, PSIM_MSG_TABLE,
+                           (int64_t)t);
+  }
+
+  std::vector<int64_t> box_offsets(size_t bi) const {
+    std::vector<int64_t> off(g->n_pf + 1);
+    for (int f = 0; f <= g->n_pf; ++f) off[f] = n_out[bi] * f / g->n_pf;
+    return off;
+  }
+
+  // The comm schedule alone (psim_run_comms): execute()'s groups, in order.
+  void comm_trace() {
+    if (g->n_pf > 1) field_allgather(s_own, sum_parts, n_vp * esz, 2, n_vp, PSIM_MSG_SUMS, p_v);
+    blocks_group();
+    std::vector<bool> done(tabs.size(), false);
+    for (size_t bi = 0; bi < boxes.size(); ++bi) {
+      const Box& b = boxes[bi];
+      for (size_t t = 0; t < tabs.size(); ++t) {
+        const Tab& T = tabs[t];
+        const bool used = (T.X == b.A && T.Y == b.B) || (T.X == b.A && T.Y == b.C) ||
+                          (T.X == b.B && T.Y == b.C);
+        if (!used || done[t]) continue;
+        if (g->n_pf > 1) table_group(t, tab_parts);
+        done[t] = true;
+      }
+      if (n_out[bi] == 0 || g->n_pf == 1) continue;
+      field_scatter(part, rbuf, box_offsets(bi), 5, PSIM_MSG_BOX, (int64_t)bi);
+    }
+  }
+
   bool execute(psim_out_t* out) {
     if (!begin() || !load(false)) return false;
     if (validate && !S.cuda(psim::check_block(dtype, own, n_fp, n_vp, own_ld, dflags, st), "check"))
       return false;
     if (!sums()) return false;
-    const Nccl* N = g->n_pv > 1 ? &nccl() : nullptr;
+    if (g->n_pv > 1 && (!S.cuda(cudaEventRecord(ev_tmp, st), "event") ||
+                        !S.cuda(cudaStreamWaitEvent(ctx->cstream, ev_tmp, 0), "wait")))
+      return false;
     // the block circulation (metrics3.py:93-109, face_j / vol_k / vol_j) as one
     // circulant all-gather of blocks and sums on the comm stream, overlapped
     // with the diagonal-edge boxes that need only the own block
-    if (g->n_pv > 1) {
-      if (!S.cuda(cudaEventRecord(ev_tmp, st), "event") ||
-          !S.cuda(cudaStreamWaitEvent(ctx->cstream, ev_tmp, 0), "wait"))
-        return false;
-      S.nc(N->GroupStart(), "ncclGroupStart");
-      for (int d = 1; d < g->n_pv; ++d) {
-        const int to = rank_of(p_f, (p_v - d + g->n_pv) % g->n_pv, p_r);
-        const int fs = (p_v + d) % g->n_pv;
-        const int from = rank_of(p_f, fs, p_r);
-        S.nc(N->Send(own, n_vp * ld * esz, ncclChar, to, ctx->comm, ctx->cstream), "ncclSend");
-        S.nc(N->Send(s_own, n_vp * esz, ncclChar, to, ctx->comm, ctx->cstream), "ncclSend");
-        S.nc(N->Recv(blocks[fs], n_vp * ld * esz, ncclChar, from, ctx->comm, ctx->cstream),
-             "ncclRecv");
-        S.nc(N->Recv(bsums[fs], n_vp * esz, ncclChar, from, ctx->comm, ctx->cstream), "ncclRecv");
-        count_send(0, n_fp * n_vp, n_fp * n_vp * esz);
-        count_send(2, n_vp, n_vp * esz);
-      }
-      if (!S.nc(N->GroupEnd(), "ncclGroupEnd")) return false;
-    }
+    if (!blocks_group()) return false;
     bool gathered = g->n_pv == 1;
     std::vector<bool> tab_done(tabs.size(), false);
     for (size_t bi = 0; bi < boxes.size(); ++bi) {
@@ -1011,8 +1087,7 @@ struct Run3 : Rank {
                                T.X == T.Y, dst, n_vp, 0, st)))
           return false;
         if (g->n_pf > 1) {
-          if (!field_allgather(dst, tab_parts, n_vp * n_vp * esz, 4, n_vp * n_vp)) return false;
-          // field_allgather copies `mine` onto its own slot first: same buffer, harmless
+          if (!table_group(t, dst)) return false;
           if (!fold_parts(T.data, tab_parts, n_vp * n_vp)) return false;
         }
         tab_done[t] = true;
@@ -1031,28 +1106,9 @@ struct Run3 : Rank {
       // reduce-scatter over the field group, then values for this rank's range
       psim_box3_t raw = box_struct(b, part, false);
       if (!kmark() || !S.psim(psim_czek3_box_numerators(dtype, &raw, st)) || !kmark()) return false;
-      const int64_t no = n_out[bi];
-      std::vector<int64_t> off(g->n_pf + 1);
-      for (int f = 0; f <= g->n_pf; ++f) off[f] = no * f / g->n_pf;
+      const std::vector<int64_t> off = box_offsets(bi);
       const int64_t mine = off[p_f + 1] - off[p_f];
-      char* rb = static_cast<char*>(rbuf);
-      const Nccl& NN = nccl();
-      S.nc(NN.GroupStart(), "ncclGroupStart");
-      for (int f = 0; f < g->n_pf; ++f) {
-        const int64_t sz = (off[f + 1] - off[f]) * esz;
-        if (f == p_f) {
-          S.cuda(cudaMemcpyAsync(rb + f * mine * esz, static_cast<char*>(part) + off[f] * esz, sz,
-                                 cudaMemcpyDeviceToDevice, st), "stage part");
-          continue;
-        }
-        const int peer = rank_of(f, p_v, p_r);
-        if (sz) S.nc(NN.Send(static_cast<char*>(part) + off[f] * esz, sz, ncclChar, peer, ctx->comm, st),
-                     "ncclSend");
-        if (mine) S.nc(NN.Recv(rb + f * mine * esz, mine * esz, ncclChar, peer, ctx->comm, st),
-                       "ncclRecv");
-        if (sz) count_send(5, off[f + 1] - off[f], sz);
-      }
-      if (!S.nc(NN.GroupEnd(), "ncclGroupEnd")) return false;
+      if (!field_scatter(part, rbuf, off, 5, PSIM_MSG_BOX, (int64_t)bi)) return false;
       if (mine == 0) continue;
       if (!fold_parts(tot, rbuf, mine)) return false;
       psim_box3_t s = box_struct(b, nullptr, true);
@@ -1069,7 +1125,8 @@ struct Run3 : Rank {
 template <class R>
 int plan_or_run(psim_ctx* ctx, const psim_problem_t* p, const psim_grid_t* g, int stage, int flags,
                 void* ws, int64_t ws_bytes, psim_out_t* out, void* stream, psim_plan_t* plan,
-                psim_piece_t* plan_pieces = nullptr, int64_t cap = 0) {
+                psim_piece_t* plan_pieces = nullptr, int64_t cap = 0,
+                std::vector<psim_msg_t>* comms = nullptr) {
   R r;
   r.ctx = ctx;
   r.pr = p;
@@ -1080,6 +1137,12 @@ int plan_or_run(psim_ctx* ctx, const psim_problem_t* p, const psim_grid_t* g, in
   // dry layout: sizes only
   r.A.dry = true;
   r.layout(out);
+  if (comms) {  // the message schedule only
+    r.trace = true;
+    r.comm_trace();
+    *comms = r.log;
+    return PSIM_OK;
+  }
   if (plan) {
     plan->n_pieces = (int64_t)r.pieces.size();
     plan->n_vals = r.n_vals;
@@ -1201,6 +1264,26 @@ int psim_run_pieces(const psim_ctx* ctx, const psim_problem_t* p, const psim_gri
                                  cap);
 }
 
+int psim_run_comms(const psim_ctx* ctx, const psim_problem_t* p, const psim_grid_t* g, int stage,
+                   int flags, psim_msg_t* msgs, int64_t cap, int64_t* n) {
+  if (!n) return set_error(PSIM_ECONFIG, "NULL count");
+  if (int r = check_common(ctx, p, g, p ? p->arity : 0)) return r;
+  if (p->arity != 2 && p->arity != 3) return set_error(PSIM_ECONFIG, "arity must be 2 or 3");
+  if (p->arity == 3 && (stage < -1 || stage >= g->n_st))
+    return set_error(PSIM_ECONFIG, "stage %d outside [0, %d)", stage, g->n_st);
+  std::vector<psim_msg_t> log;
+  psim_ctx* c = const_cast<psim_ctx*>(ctx);
+  const int r = p->arity == 2
+                    ? plan_or_run<Run2>(c, p, g, -1, flags, nullptr, 0, nullptr, nullptr, nullptr,
+                                        nullptr, 0, &log)
+                    : plan_or_run<Run3>(c, p, g, stage, flags, nullptr, 0, nullptr, nullptr,
+                                        nullptr, nullptr, 0, &log);
+  if (r) return r;
+  *n = (int64_t)log.size();
+  if (msgs) std::copy(log.begin(), log.begin() + std::min<int64_t>(cap, *n), msgs);
+  return PSIM_OK;
+}
+
 int psim_run2(psim_ctx* ctx, const psim_problem_t* p, const psim_grid_t* g, int flags, void* ws,
               int64_t ws_bytes, psim_out_t* out, void* stream) {
   if (int r = check_common(ctx, p, g, 2)) return r;
@@ -1221,6 +1304,30 @@ int psim_run3(psim_ctx* ctx, const psim_problem_t* p, const psim_grid_t* g, int 
   if (ctx->world > 1 && nccl().error) return set_error(PSIM_ERUNTIME, "%s", nccl().error);
   cudaSetDevice(ctx->device);
   return plan_or_run<Run3>(ctx, p, g, stage, flags, ws, ws_bytes, out, stream, nullptr);
+}
+
+int psim_malloc(void** ptr, int64_t bytes, int pinned_host) {
+  if (!ptr || bytes < 0) return set_error(PSIM_ECONFIG, "bad allocation request");
+  *ptr = nullptr;
+  if (bytes == 0) return PSIM_OK;
+  cudaError_t e = pinned_host ? cudaHostAlloc(ptr, bytes, cudaHostAllocDefault)
+                              : cudaMalloc(ptr, bytes);
+  if (e != cudaSuccess)
+    return set_error(PSIM_ERUNTIME, "allocation of %lld bytes failed: %s", (long long)bytes,
+                     cudaGetErrorString(e));
+  return PSIM_OK;
+}
+
+int psim_free(void* ptr, int pinned_host) {
+  if (!ptr) return PSIM_OK;
+  cudaError_t e = pinned_host ? cudaFreeHost(ptr) : cudaFree(ptr);
+  return e == cudaSuccess ? PSIM_OK : set_error(PSIM_ERUNTIME, "free: %s", cudaGetErrorString(e));
+}
+
+int psim_memcpy(void* dst, const void* src, int64_t bytes) {
+  if (bytes < 0 || (bytes && (!dst || !src))) return set_error(PSIM_ECONFIG, "bad copy");
+  cudaError_t e = cudaMemcpy(dst, src, bytes, cudaMemcpyDefault);
+  return e == cudaSuccess ? PSIM_OK : set_error(PSIM_ERUNTIME, "copy: %s", cudaGetErrorString(e));
 }
 
 int psim_checksum(int dtype, const void* vals, const int64_t* idx, int64_t idx0, int64_t count,

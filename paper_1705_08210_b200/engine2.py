@@ -11,8 +11,8 @@ Transports:
   "local"  every rank of the grid runs on this process's current GPU, one
            after another; "exchanges" are reads of blocks already in HBM.
            (The reference's "thread" / "process" transports map here.)
-  "nccl"   one process per GPU (torch.distributed, NCCL backend,
-           world_size == grid.n_p): see dist.py.
+  "nccl"   one process per GPU: libpsim's run-level runtime (psim_run2,
+           csrc/runtime.cu; runtime.py), world_size == grid.n_p.
 """
 from __future__ import annotations
 

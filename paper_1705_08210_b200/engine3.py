@@ -67,26 +67,6 @@ class Tables:
         return self.cache[key]
 
 
-class FieldFoldedTables:
-    """NCCL field split: this rank's slab table, all-gathered over the field
-    group and folded in ascending p_f (every field rank computes the same
-    folded table; all field ranks request tables in the same order)."""
-
-    def __init__(self, blocks: dict, code: int, group, n_pf: int):
-        self.local = Tables(blocks, code)
-        self.code, self.group, self.n_pf = code, group, n_pf
-        self.cache: dict = {}
-
-    def __call__(self, X: int, Y: int) -> torch.Tensor:
-        if (X, Y) not in self.cache:
-            from .dist import fold_over_field
-
-            part = self.local(X, Y)
-            self.cache[X, Y] = fold_over_field(part, self.code, self.group, self.n_pf)
-            del self.local.cache[X, Y]
-        return self.cache[X, Y]
-
-
 class FoldedTables:
     """Numerator tables over a field split: each field slab's table, folded in
     ascending p_f order (the reference reduces P_bc and the per-pivot
@@ -224,177 +204,6 @@ def run_local(problem, grid, stages, keep_values: bool = True,
     lo, hi, deg = D.acc_words(acc)
     all_sums = D.to_host(torch.cat([sums[p] for p in range(grid.n_pv)]))
     return Outcome(pieces, lo, hi, deg, count, all_sums, start.elapsed_time(end) * 1e-3)
-
-
-class Runner3Dist:
-    """One rank's 3-way pipeline over NCCL (one process per GPU, n_pf = 1).
-
-    Blocks circulate as in the reference's face_j / vol_k / vol_j exchanges
-    (schedule.py:196-213), but each block is received once and cached
-    (the whole input of cfg4 is 480 MB): a circulant all-gather inside the
-    replica group, posted before the diagonal-edge units so the transfers
-    overlap their compute. Then every face / volume unit of the plan runs
-    as boxes. With ``out_budget`` set, box values go to one reused HBM
-    buffer (bench mode: values are still computed and stored)."""
-
-    kernel_name = "k_czek3<T> (psim_czek3_box)"
-
-    def __init__(self, problem, grid, stages, keep_values: bool = True,
-                 out_budget: float | None = None):
-        from .dist import ensure_initialized, field_group
-
-        self.world, self.rank = ensure_initialized(grid)
-        from .domain import coords_of_rank
-
-        self.problem, self.grid, self.stages = problem, grid, tuple(stages)
-        self.keep, self.out_budget = keep_values, out_budget
-        self.coords = coords_of_rank(self.rank, grid)
-        self.group = field_group(grid, self.coords)
-        self.code = D.code_of(problem.precision)
-        self.n_vp = problem.n_v // grid.n_pv
-        units = [e for e in plan_3way(grid, self.coords) if isinstance(e, Unit3)]
-        edge, rest = [], []
-        for u in units:
-            (edge if u.cls == "edge" else rest).extend(
-                unit_boxes(u, self.n_vp, grid.n_st, self.stages))
-        self.edge_boxes, self.rest_boxes = merge_boxes(edge), merge_boxes(rest)
-        from .plan import box_count
-
-        nb = len(self.edge_boxes) + len(self.rest_boxes)
-        work = sum(box_count(b) for b in self.edge_boxes + self.rest_boxes)
-        self.my_cmp = work * problem.n_f
-        self.kernel_cmp_per_launch = self.my_cmp / max(1, nb)
-
-    def peer(self, slab: int) -> int:
-        from .domain import rank_of_coords
-
-        c = self.coords
-        return rank_of_coords(RankCoords(c.p_f, slab % self.grid.n_pv, c.p_r), self.grid)
-
-    def setup(self) -> None:
-        import torch.distributed  # noqa: F401
-
-        dev = torch.device("cuda", torch.cuda.current_device())
-        self.dev = dev
-        p, g = self.problem, self.grid
-        own = D.load_block(p, g, self.coords, dev)
-        self.blocks = {self.coords.p_v: own}
-        for d in range(1, g.n_pv):
-            slab = (self.coords.p_v + d) % g.n_pv
-            self.blocks[slab] = D.Block(torch.empty_like(own.data), own.n_fp, own.n_vp, own.ld,
-                                        slab * self.n_vp, p.precision)
-        self.sums = {s: torch.empty(self.n_vp, dtype=own.data.dtype, device=dev)
-                     for s in self.blocks}
-        if g.n_pf == 1:
-            self.tables = Tables(self.blocks, self.code)
-        else:
-            self.tables = FieldFoldedTables(self.blocks, self.code, self.group, g.n_pf)
-        self.acc = D.new_acc(dev)
-        self.buf = None
-        if self.out_budget is not None and g.n_pf == 1:
-            sizes = [box_plan(self._struct(b, None))[0] for b in self.edge_boxes + self.rest_boxes]
-            self.buf = torch.empty(max(sizes + [1]), dtype=D.torch_dtype(p.precision), device=dev)
-
-    def _struct(self, box, vals):
-        p = self.problem
-        return box_struct(box, self.blocks, self.sums, self.tables, p.n_f, p.n_v, vals, self.acc)
-
-    def _run_field(self, boxes):
-        """Field split: raw n_ijk of this slab -> ordered reduce-scatter over the
-        field group -> values for this rank's element share."""
-        from .dist import reduce_scatter_flat
-
-        p, g = self.problem, self.grid
-        tdt = D.torch_dtype(p.precision)
-        for box in boxes:
-            n_out, _ = box_plan(self._struct(box, None))
-            if n_out == 0:
-                continue
-            part = torch.empty(n_out, dtype=tdt, device=self.dev)
-            raw = box_struct(box, self.blocks, None, None, self.blocks[box.blocks[0]].n_fp, p.n_v,
-                             part, self.acc)
-            N.call("psim_czek3_box_numerators", self.code, C.byref(raw), D.stream_ptr())
-            total, e0, e1 = reduce_scatter_flat(part, self.coords.p_f, g.n_pf, self.group,
-                                                lambda d, s: D.fold_(d, s, self.code))
-            vals = torch.empty(e1 - e0, dtype=tdt, device=self.dev) if self.keep else None
-            b = self._struct(box, None)
-            if e1 > e0:
-                N.call("psim_czek3_from_numerators", self.code, C.byref(b), D.ptr(total), e0, e1,
-                       D.ptr(vals), D.stream_ptr())
-            self.pieces.append(BoxPiece(box.i0, box.i1, box.j0, box.j1, box.k0, box.k1, vals,
-                                        e0, e1))
-            self.count += e1 - e0
-
-    def _run(self, boxes, timed, events):
-        if self.grid.n_pf > 1:
-            return self._run_field(boxes)
-        tdt = D.torch_dtype(self.problem.precision)
-        for box in boxes:
-            n_out, _ = box_plan(self._struct(box, None))
-            if n_out == 0:
-                continue
-            if self.buf is not None:
-                vals = self.buf[:n_out]
-            else:
-                vals = torch.empty(n_out, dtype=tdt, device=self.dev) if self.keep else None
-            b = self._struct(box, vals)
-            if timed:
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
-            N.call("psim_czek3_box", self.code, C.byref(b), D.stream_ptr())
-            if timed:
-                e1.record()
-                events.append((e0, e1))
-            if self.buf is None:
-                self.pieces.append(BoxPiece(box.i0, box.i1, box.j0, box.j1, box.k0, box.k1, vals))
-            self.count += n_out
-
-    def step(self, timed: bool = False) -> list:
-        import torch.distributed as dist
-
-        g, me = self.grid, self.coords.p_v
-        self.acc.zero_()
-        self.pieces, self.count = [], 0
-        own = self.blocks[me]
-        s = D.column_sums(own)
-        if g.n_pf > 1:
-            from .dist import fold_over_field
-
-            s = fold_over_field(s, self.code, self.group, g.n_pf)
-        self.sums[me].copy_(s)
-        self.tables.cache.clear()
-        works = []
-        if g.n_pv > 1:
-            from .dist import allgather_ops
-
-            data = {slab: b.data for slab, b in self.blocks.items()}
-            works = dist.batch_isend_irecv(allgather_ops(me, g.n_pv, data, self.sums, self.peer))
-        events: list = []
-        self._run(self.edge_boxes, timed, events)
-        for w in works:
-            w.wait()
-        self._run(self.rest_boxes, timed, events)
-        return events
-
-    def totals(self):
-        from .dist import gather_totals
-
-        return gather_totals(self.acc, self.count, self.world, self.dev)
-
-    def checksum_hex(self) -> str:
-        from .synthetic import Checksum128
-
-        lo, hi, _, _ = self.totals()
-        return Checksum128.from_words(lo, hi).hex
-
-    def global_sums(self):
-        return D.to_host(torch.cat([self.sums[s] for s in range(self.grid.n_pv)]))
-
-    def teardown(self) -> None:
-        for name in ("blocks", "sums", "tables", "acc", "buf", "pieces"):
-            if hasattr(self, name):
-                delattr(self, name)
-        torch.cuda.empty_cache()
 
 
 class Resident3:
