@@ -603,7 +603,28 @@ def e2e_2way(P, prob, grid, precision, args, total_cmp, world, rank) -> dict:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         el = float(t.item())
     isz = 8 if precision == "double" else 4
+    pageable = None
+    if world == 1 and not args.no_pageable:
+        # the same run from a plain numpy (pageable) block -- the reference's
+        # ArraySource (tests/conftest.py:17-26): staged through a pinned ring
+        # chunk by chunk under the streamed kernel
+        src_p = SlabSource(np.asfortranarray(host.numpy().T.copy()), coords)
+        prob_p = P.Problem(2, prob.n_f, prob.n_v, src_p, precision)
+        P.run_2way(prob_p, grid, transport=transport, host_values=True)  # warm-up
+        tp = []
+        for _ in range(steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            res = P.run_2way(prob_p, grid, transport=transport, host_values=True)
+            tp.append(time.perf_counter() - t0)
+            assert res.checksum.hex == cks
+        pageable = {"value": total_cmp / statistics.median(tp), "unit": "comparisons/s",
+                    "seconds_per_step": statistics.median(tp),
+                    "api": "run_2way(Problem(2, n_f, n_v, numpy pageable slab source), grid, "
+                           "host_values=True)"}
+        del src_p, prob_p
     return {"value": total_cmp / el, "unit": "comparisons/s",
+            "pageable_source": pageable,
             "h2d_bytes_per_step": prob.n_f * prob.n_v * isz,
             "d2h_bytes_per_step": math.comb(prob.n_v, 2) * isz + 32 * world,
             "seconds_per_step": el, "checksum": cks,
@@ -792,6 +813,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-pageable", action="store_true")
     ap.add_argument("--launch-check", action="store_true",
                     help="CPU check of the multi-rank launch (gloo): print the world and plan")
     args = ap.parse_args()

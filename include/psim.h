@@ -172,10 +172,12 @@ int psim_min_columns(int dtype, const void* V, int64_t n_fp, int64_t n_vp, int64
  * column sums. No row bands. */
 int psim_sorenson2_block(int dtype, const psim_block2_t* task, void* stream);
 /* One whole diagonal task (the single-slab run, metrics2.py:149-158) over a
- * block still in PINNED host memory (vector i at host + i*host_ld elements):
- * the block is copied into task->W (== task->V, device, padded ld) by the
- * copy engine on copy_stream in chunks of `chunk` vectors from the last one
- * down, each followed by ready[c] = 1; the fused kernel on compute_stream
+ * block still in host memory (vector i at host + i*host_ld elements): the
+ * block is copied into task->W (== task->V, device, padded ld) by the copy
+ * engine on copy_stream in chunks of `chunk` vectors from the last one down,
+ * each followed by ready[c] = 1 (pageable memory is staged chunk by chunk
+ * through a pinned ring by host threads; the call then returns once the last
+ * chunk is uploaded); the fused kernel on compute_stream
  * starts at the bottom tiles as soon as their chunk lands. The column sums
  * come from one extra CTA per row tile placed at the head of its bottom-up
  * band: it folds its 128 vectors' sums (k_colsum's sequential order), WRITES

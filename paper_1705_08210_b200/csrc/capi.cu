@@ -289,10 +289,9 @@ int psim_czek2_streamed(int dtype, const psim_block2_t* t, const void* host, int
                 (long long)psim::kStreamMaxFlags);
   if (compute_stream == copy_stream) return fail(PSIM_ECONFIG, "copy stream must differ");
   cudaPointerAttributes pa{};
-  if (cudaPointerGetAttributes(&pa, host) != cudaSuccess || pa.type != cudaMemoryTypeHost) {
-    cudaGetLastError();
-    return fail(PSIM_ECONFIG, "host block must be pinned (page-locked) memory");
-  }
+  if (cudaPointerGetAttributes(&pa, host) == cudaSuccess && pa.type == cudaMemoryTypeDevice)
+    return fail(PSIM_ECONFIG, "host block is device memory");
+  cudaGetLastError();
   return cuda_status(psim::czek2_streamed(dtype, *t, host, host_ld, chunk, ready,
                                           S(compute_stream), S(copy_stream)),
                      "psim_czek2_streamed");

@@ -16,6 +16,11 @@
 // task's ragged last row tile as a 32-row edge task (czek2_tasks_t).
 #include <cstdlib>
 
+#include <cstring>
+#include <mutex>
+#include <thread>
+#include <vector>
+
 #include "minplus.cuh"
 #include "psim_internal.h"
 
@@ -656,6 +661,92 @@ static cudaError_t flag_sources(const unsigned** zeros, const unsigned** one) {
   return st;
 }
 
+// Pageable host input of a streamed run: each chunk (last first) is copied
+// by host threads into a slot of a pinned ring, then uploaded from there by
+// the copy engine (one cudaMemcpyAsync per chunk) and flagged; a slot is
+// reused once its upload has completed. The host thread returns when the last
+// chunk is enqueued -- the kernel, launched before, computes meanwhile.
+namespace {
+constexpr int kRing = 4;
+struct PinnedRing {
+  std::mutex mu;
+  char* buf[kRing] = {};
+  cudaEvent_t done[kRing] = {};
+  size_t cap = 0;
+};
+PinnedRing& ring() {
+  static PinnedRing r;  // grown on demand, kept for the process (pinning is slow)
+  return r;
+}
+
+cudaError_t spin_event(cudaEvent_t ev) {  // (blocking waits wake late on these boxes)
+  for (;;) {
+    const cudaError_t e = cudaEventQuery(ev);
+    if (e != cudaErrorNotReady) return e;
+  }
+}
+
+void copy_rows(char* dst, int64_t dst_ld, const char* src, int64_t src_ld, int64_t row_bytes,
+               int64_t rows) {
+  const int64_t total = rows * row_bytes;
+  const int nt = total > (16 << 20) ? 4 : 1;
+  auto part = [&](int k) {
+    for (int64_t r = rows * k / nt; r < rows * (k + 1) / nt; ++r)
+      std::memcpy(dst + r * dst_ld, src + r * src_ld, row_bytes);
+  };
+  std::vector<std::thread> th;
+  for (int k = 1; k < nt; ++k) th.emplace_back(part, k);
+  part(0);
+  for (auto& x : th) x.join();
+}
+}  // namespace
+
+static cudaError_t stage_pageable(void* dst_, int64_t ldw, const void* src_, int64_t host_ld,
+                                  int64_t n_f, int64_t n, int64_t chunk, size_t sz,
+                                  unsigned* ready, const unsigned* one, int64_t nflags,
+                                  cudaStream_t copy) {
+  PinnedRing& R = ring();
+  std::lock_guard<std::mutex> lock(R.mu);
+  const size_t need = (size_t)chunk * ldw * sz;
+  cudaError_t e = cudaSuccess;
+  if (R.cap < need) {
+    for (int k = 0; k < kRing; ++k) {
+      if (R.buf[k]) cudaFreeHost(R.buf[k]);
+      R.buf[k] = nullptr;
+    }
+    R.cap = 0;
+    for (int k = 0; k < kRing && e == cudaSuccess; ++k) {
+      e = cudaHostAlloc(&R.buf[k], need, cudaHostAllocDefault);
+      if (e == cudaSuccess && !R.done[k])
+        e = cudaEventCreateWithFlags(&R.done[k], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) R.cap = need;
+  }
+  char* dst = static_cast<char*>(dst_);
+  const char* src = static_cast<const char*>(src_);
+  const int64_t nchunks = (n + chunk - 1) / chunk;
+  int64_t i = 0;
+  for (int64_t c = nchunks - 1; c >= 0 && e == cudaSuccess; --c, ++i) {
+    const int slot = (int)(i % kRing);
+    if (i >= kRing) e = spin_event(R.done[slot]);  // its previous upload is done
+    if (e != cudaSuccess) break;
+    const int64_t lo = c * chunk, rows = min64(n, lo + chunk) - lo;
+    copy_rows(R.buf[slot], ldw * sz, src + lo * host_ld * sz, host_ld * sz, n_f * sz, rows);
+    e = cudaMemcpyAsync(dst + lo * ldw * sz, R.buf[slot], rows * ldw * sz,
+                        cudaMemcpyHostToDevice, copy);
+    if (e == cudaSuccess) e = cudaEventRecord(R.done[slot], copy);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(ready + c, one, sizeof(unsigned), cudaMemcpyHostToDevice, copy);
+  }
+  if (e != cudaSuccess)  // release every flag: the kernel finishes, the error discards it
+    for (int64_t k = 0; k < nflags; ++k)
+      cudaMemcpyAsync(ready + k, one, sizeof(unsigned), cudaMemcpyHostToDevice, copy);
+  // the ring must not be refilled before this run's last uploads are done
+  for (int k = 0; k < kRing && e == cudaSuccess; ++k)
+    if (R.done[k]) e = spin_event(R.done[k]);
+  return e;
+}
+
 template <typename T>
 cudaError_t czek2_streamed_t(const Czek2Block& t, const void* host, int64_t host_ld,
                              int64_t chunk, unsigned* ready, cudaStream_t compute,
@@ -694,6 +785,12 @@ cudaError_t czek2_streamed_t(const Czek2Block& t, const void* host, int64_t host
     return e;
   T* dst = static_cast<T*>(const_cast<void*>(t.W));
   const T* src = static_cast<const T*>(host);
+  cudaPointerAttributes pa{};
+  const bool pinned = cudaPointerGetAttributes(&pa, host) == cudaSuccess &&
+                      pa.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  if (!pinned)  // pageable: staged through a pinned ring, chunk by chunk
+    return stage_pageable(dst, t.ldw, src, host_ld, t.n_f, n, chunk, sz, ready, one, nflags, copy);
   for (int64_t c = nchunks - 1; c >= 0; --c) {
     const int64_t lo = c * chunk, hi = min64(n, lo + chunk);
     e = host_ld == t.ldw  // same pitch: the chunk is one contiguous span

@@ -648,15 +648,10 @@ struct Run2 : Rank {
       rblock.push_back(A.take(n_vp * ld * esz));
       rsums.push_back(A.take(n_vp * esz));
     }
-    // pinned host input with a diagonal task on this rank: streamed upload
+    // host input (pinned, or pageable staged through a pinned ring) with a
+    // diagonal task on this rank: streamed upload under the diagonal kernel
     streamed = pr->input == PSIM_INPUT_HOST && g->n_pf == 1 && !(flags & PSIM_RUN_NO_STREAM) &&
                n_vp >= 2 && !tasks.empty() && tasks[0].diag();
-    if (streamed) {
-      cudaPointerAttributes pa{};
-      if (cudaPointerGetAttributes(&pa, pr->block) != cudaSuccess || pa.type != cudaMemoryTypeHost)
-        streamed = false;  // pageable host memory: plain upload
-      cudaGetLastError();
-    }
     if (streamed) {
       int bm = 0, bn = 0;
       psim::tile_shape(dtype, &bm, &bn);

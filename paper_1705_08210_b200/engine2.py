@@ -144,9 +144,12 @@ def finish_numerators(code, N, r0, r1, m, n, diagonal, s_row, s_col, g_row, g_co
 _COPY_STREAM: dict = {}
 
 
-def pinned_host_block(problem, grid, coords=None):
-    """A rank's block (default: the single slab) as a pinned (n_vp, n_fp) host
-    tensor when the source hands out pinned memory (no copy), else None."""
+def host_stream_block(problem, grid, coords=None):
+    """A generic source's block (default: the single slab) as an (n_vp, n_fp)
+    host tensor over the same bytes, for the streamed run: pinned memory is
+    uploaded by the copy engine directly, pageable memory is staged through a
+    pinned ring chunk by chunk (psim_czek2_streamed). None for synthetic and
+    vector-file sources (generated / streamed to the device elsewhere)."""
     import os
 
     from .domain import host_block
@@ -159,8 +162,7 @@ def pinned_host_block(problem, grid, coords=None):
     if synthetic_kind(src) is not None or is_vector_file(src):
         return None
     arr = host_block(problem, grid, coords or RankCoords(0, 0, 0))  # (n_fp, n_vp) Fortran
-    host = torch.from_numpy(np.ascontiguousarray(arr.T))  # (n_v, n_f), same bytes
-    return host if host.is_pinned() else None
+    return torch.from_numpy(np.ascontiguousarray(arr.T))  # (n_v, n_f), same bytes
 
 
 # PSIM_TRACE=1: run_streamed records CUDA events (and host clocks) at its
@@ -193,11 +195,11 @@ def stream_chunk(n: int) -> int:
 
 
 def run_streamed(problem, host: torch.Tensor, keep_values: bool, sink) -> Outcome:
-    """Single-slab run whose input is still in pinned host memory: the copy
-    engine uploads the block in chunks (last vectors first) while the fused
-    kernel starts on the bottom tiles (psim_czek2_streamed), so the H2D copy
-    is hidden behind the compute instead of preceding it; the column sums come
-    out of the kernel. The block is validated (finite, >= 0) once it has
+    """Single-slab run whose input is still in host memory (pinned, or
+    pageable staged through a pinned ring): the copy engine uploads the block
+    in chunks (last vectors first) while the fused kernel starts on the bottom
+    tiles (psim_czek2_streamed), so the H2D copy is hidden behind the compute
+    instead of preceding it; the column sums come out of the kernel. The block is validated (finite, >= 0) once it has
     landed -- before the result is returned."""
     import ctypes as C
 
@@ -251,7 +253,7 @@ def run_local(problem, grid, balance: str = "split", keep_values: bool = True,
     bitpacked = bitpacked and grid.n_pf == 1
     code = D.code_of(problem.precision)
     if n_ranks(grid) == 1 and not bitpacked and (sink is None or sink.direct):
-        host = pinned_host_block(problem, grid)
+        host = host_stream_block(problem, grid)
         if host is not None:
             return run_streamed(problem, host, keep_values, sink)
     n_vp = problem.n_v // grid.n_pv

@@ -576,3 +576,24 @@ def test_full_cfg2_sampled_parity():
     assert par["mismatches"] == 0, par
     assert r.checksum_hex() == "73cac6d75612b5f4372130e4fd66716c"
     r.teardown()
+
+
+def test_pageable_source_streams_through_pinned_ring():
+    """A plain numpy source (pageable memory, the reference's ArraySource) on
+    the single-slab path: chunks are staged through the pinned ring while the
+    streamed kernel runs (12 chunks through 4 slots); values and checksum
+    equal the run on the device-generated block, and invalid data still
+    raises DataError."""
+    from oracle import propsim_np as O
+
+    P = _api()
+    n_f, n_v = 777, 3000
+    m = O.uniform(6, n_f, n_v, np.float64)
+    want = P.run_2way(P.Problem(2, n_f, n_v, P.gen_uniform(6, n_f, n_v)), P.DecompGrid())
+    got = P.run_2way(P.Problem(2, n_f, n_v, ArraySource(np.asfortranarray(m))), P.DecompGrid())
+    assert got.checksum == want.checksum
+    assert (got.records.values.view(np.uint64) == want.records.values.view(np.uint64)).all()
+    bad = np.asfortranarray(m.copy())
+    bad[10, 2999] = -1.0
+    with pytest.raises(P.DataError):
+        P.run_2way(P.Problem(2, n_f, n_v, ArraySource(bad)), P.DecompGrid())
