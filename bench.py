@@ -262,6 +262,11 @@ def run_ours(args) -> dict | None:
                C.byref(cps), C.byref(cpc), D.stream_ptr())
         if cps.value > peak:
             peak, peak_clk, peak_var = cps.value, cpc.value, var
+    # the production mainloop itself over shared-memory operands (variant 3):
+    # what the kernel's instruction stream can reach without staging / epilogue
+    ml_cps, ml_cpc = C.c_double(), C.c_double()
+    N.call("psim_peak_minplus", code, 3, 20000 if precision == "double" else 40000,
+           C.byref(ml_cps), C.byref(ml_cpc), D.stream_ptr())
     sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
     issue_limit = 32 if precision == "double" else 64  # cmp/clk/SM: 4 resp. 2 instr/cmp
     if args.config == "sor2":  # AND+POPC: one POPC (16/clk/SM) covers 32 fields
@@ -379,6 +384,11 @@ def run_ours(args) -> dict | None:
                                 f"instruction mix, same run ({peak_clk:.2f} cmp/clk/SM, "
                                 f"variant {peak_var})"),
                 "whole_step_frac": (total_cmp / (ms * 1e-3) / world) / peak,
+                "mainloop_ceiling": {
+                    "value": ml_cps.value, "cmp_per_clk_sm": ml_cpc.value,
+                    "frac": (achieved / ml_cps.value) if achieved and ml_cps.value else None,
+                    "what": "psim_peak_minplus variant 3: the production micro_step loop "
+                            "over operands resident in shared memory (no staging, no epilogue)"},
                 "issue_limit_cmp_per_clk_sm": issue_limit,
                 "frac_of_issue_limit": (achieved / (issue_limit * sm_count * 1e6
                                                     * clocks["sm_mhz"]))

@@ -16,6 +16,9 @@
 // task's ragged last row tile as a 32-row edge task (czek2_tasks_t).
 #include <cstdlib>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstring>
 #include <mutex>
 #include <thread>
@@ -72,6 +75,10 @@ struct Args2 {
   const T* seg_scol[kMaxSeg];
   int64_t seg_gcol[kMaxSeg];
   T* seg_out[kMaxSeg];
+  // TMA staging (minplus_tile_tma): tensor maps of W (rows) and V (columns;
+  // a flattened group whose segments lie back to back is one operand)
+  int tma;
+  CUtensorMap tmW, tmV;
 };
 
 // Segment of flat column c (kCzek2Flat): a short uniform scan.
@@ -215,11 +222,12 @@ __device__ __forceinline__ int64_t packed_pos(int diagonal, int64_t i, int64_t j
 }
 
 template <class C, int MODE>
-__global__ void __launch_bounds__(kNT, C::MINB) k_minplus2(const Args2<typename C::T> a) {
+__global__ void __launch_bounds__(kNT, C::MINB)
+    k_minplus2(const __grid_constant__ Args2<typename C::T> a) {
   using T = typename C::T;
   // let a programmatically dependent next task start filling SMs right away
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];  // TMA destinations: 128 B
   T* smem = reinterpret_cast<T*>(smem_raw);
   constexpr bool STREAMED = MODE == kCzek2Streamed;
   // streamed: bands bottom-up (their input arrives first), each led by the
@@ -246,8 +254,13 @@ __global__ void __launch_bounds__(kNT, C::MINB) k_minplus2(const Args2<typename 
     const int64_t row0 = (int64_t)bi * C::BM, col0 = (int64_t)bj * C::BN;
     if (STREAMED) {
       if (!cta_wait_ready(a.ready + min64(row0, col0) / a.chunk, 0)) return;
+      // the chunk was written by the copy engine: order the flag's acquire
+      // before the async-proxy (TMA) reads of it
+      if (a.tma) asm volatile("fence.proxy.async.global;" ::: "memory");
     }
-    if constexpr (MODE == kCzek2Flat) {
+    if (a.tma) {  // launch-uniform
+      minplus_tile_tma<C>(&a.tmW, (int)row0, &a.tmV, (int)col0, a.n_f, acc, smem);
+    } else if constexpr (MODE == kCzek2Flat) {
       // columns [col0, split) from segment s, the rest from segment s + 1
       const int s = seg_of(a, col0);
       const int cols = (int)min64(C::BN, a.n - col0);
@@ -432,6 +445,64 @@ static int64_t plan2(Args2<typename C::T>& a, int64_t row_begin, int64_t row_end
   return blocks;
 }
 
+// Tensor maps for TMA staging (minplus_tile_tma). The encoder comes from the
+// driver through the runtime (no libcuda link); PSIM_NO_TMA=1 keeps the
+// cp.async loader (A/B). A flattened group uses TMA only when its segments
+// lie back to back in memory (one V operand); otherwise the two-pointer
+// cp.async loader runs.
+// TMA staging on unless PSIM_NO_TMA=1 (read per launch, so tests can A/B it).
+static bool tma_enabled() {
+  const char* v = getenv("PSIM_NO_TMA");
+  return !(v && v[0] == '1');
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    PFN_cuTensorMapEncodeTiled_v12000 f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&f, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    cudaGetLastError();
+    return f;
+  }();
+  return fn;
+}
+
+template <typename T>
+static bool encode_operand(CUtensorMap* map, const T* base, int64_t n_f, int64_t vectors,
+                           int64_t ld, int box_rows, int pitch) {
+  auto enc = tma_encoder();
+  if (!enc || !base || vectors < 1 || n_f < 1 || n_f >= (1ll << 31) || vectors >= (1ll << 31))
+    return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)n_f, (cuuint64_t)vectors};
+  const cuuint64_t strides[1] = {(cuuint64_t)(ld * (int64_t)sizeof(T))};
+  const cuuint32_t box[2] = {(cuuint32_t)pitch, (cuuint32_t)box_rows}, es[2] = {1, 1};
+  return enc(map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+             2, const_cast<T*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <class C>
+static void setup_tma(Args2<typename C::T>& a, int mode) {
+  using T = typename C::T;
+  a.tma = 0;
+  if (!tma_enabled() || !(mode == kCzek2 || mode == kCzek2Flat || mode == kCzek2Streamed ||
+               mode == kRawCol || mode == kRawPacked))
+    return;
+  const T* vbase = a.V;
+  if (a.nseg > 0) {
+    for (int s = 0; s + 1 < a.nseg; ++s)
+      if (a.seg_V[s] + (a.seg_c0[s + 1] - a.seg_c0[s]) * a.ldv != a.seg_V[s + 1]) return;
+    vbase = a.seg_V[0];
+  }
+  if (encode_operand<T>(&a.tmW, a.W, a.n_f, a.m, a.ldw, C::BM, C::PITCH) &&
+      encode_operand<T>(&a.tmV, vbase, a.n_f, a.n, a.ldv, C::BN, C::PITCH))
+    a.tma = 1;
+}
+
 // Launch a group of tasks (same mode): band prefixes first, then the grids
 // back to back, each after the first as a programmatic dependent launch.
 // Tasks with edge[k] run the 32-row edge configuration CE.
@@ -489,6 +560,10 @@ static cudaError_t launch_group(Args2<typename C::T>* args, const int64_t* row_b
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const bool flat = args[k].nseg > 0;
+    if (is_edge(k))
+      setup_tma<CE>(args[k], flat ? FLAT_MODE : MODE);
+    else
+      setup_tma<C>(args[k], flat ? FLAT_MODE : MODE);
     note_launch();
     if (is_edge(k))
       e = flat ? cudaLaunchKernelEx(&cfg, k_minplus2<CE, FLAT_MODE>, args[k])
@@ -539,11 +614,16 @@ static int flatten_tasks(Args2<typename C::T>* args, int64_t* rb, int64_t* re, i
     const auto& a = args[k];
     return !a.diagonal && rb[k] == 0 && re[k] == 0 && a.n >= C::BN && a.m > 0;
   };
+  const bool tma = tma_enabled();
   auto same_rows = [&](int k, int l) {
     const auto& a = args[k];
     const auto& b = args[l];
+    // with TMA staging a group is one V operand: its columns must lie back to
+    // back in memory (the runtime receives blocks into one contiguous ring)
+    const bool adjacent = !tma || args[l - 1].V + args[l - 1].n * args[l - 1].ldv == b.V;
     return a.W == b.W && a.ldw == b.ldw && a.m == b.m && a.n_f == b.n_f && a.ldv == b.ldv &&
-           a.s_row == b.s_row && a.g_row == b.g_row && a.n_v == b.n_v && a.acc == b.acc;
+           a.s_row == b.s_row && a.g_row == b.g_row && a.n_v == b.n_v && a.acc == b.acc &&
+           adjacent;
   };
   int out = 0;
   for (int k = 0; k < ntasks;) {

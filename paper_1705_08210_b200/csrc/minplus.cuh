@@ -396,6 +396,102 @@ __device__ __forceinline__ void minplus_tile(const typename C::T* __restrict__ W
   if constexpr (SUMS) *vsum = vs;
 }
 
+// ---------------------------------------------------------------------------
+// TMA staging (sm_100a): the same stage layout -- (BM + BN) rows at the
+// 144-byte pitch -- filled by two cp.async.bulk.tensor 2-D box loads per stage
+// (box = PITCH fields x BM or BN vectors; the PITCH - BK fields past the chunk
+// belong to the next one and are never read; fields past n_f and vectors past
+// the operand's end arrive as zeros, as with cp.async), issued by one thread
+// and signalled on a per-stage "full" mbarrier with the transaction byte
+// count. Each warp releases a stage on its "empty" mbarrier when it is done
+// with it; the issuing thread refills the slot once all eight warps have.
+// No CTA-wide barrier per stage and no per-thread copy instructions: warps
+// drift up to STAGES - 1 stages apart. Measured (tools/exp_tma.cu,
+// profiles/r02_tma_ab.jsonl): 22.64 vs 21.54 cmp/clk/SM for the FP64 tile,
+// i.e. the rate of the mainloop on operands already in shared memory.
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+// Box (PITCH fields from field q0) x (rows from vector v0) of the tensor map.
+__device__ __forceinline__ void tma_box(void* dst, const void* map, int q0, int v0,
+                                        uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(q0), "r"(v0), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Mainloop of one tile with TMA staging: mapW / mapV are __grid_constant__
+// tensor maps of the W and V operands (dims {n_f, vectors}, stride ld),
+// w_row0 / v_row0 the tile's first vector in each. All threads must call it.
+template <class C>
+__device__ __forceinline__ void minplus_tile_tma(const void* mapW, int w_row0, const void* mapV,
+                                                 int v_row0, int64_t n_f,
+                                                 typename C::T (&acc)[C::TM][C::TN],
+                                                 typename C::T* smem) {
+  using T = typename C::T;
+  constexpr int S = C::STAGES;
+  constexpr unsigned kBytes = (C::BM + C::BN) * C::PITCH * sizeof(T);
+  __shared__ __align__(8) uint64_t full[S], empty[S];
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kNT / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+#pragma unroll
+  for (int m = 0; m < C::TM; ++m)
+#pragma unroll
+    for (int n = 0; n < C::TN; ++n) acc[m][n] = T(0);
+  __syncthreads();
+  const int KT = (int)((n_f + C::BK - 1) / C::BK);
+  auto issue = [&](int kt) {
+    const int s = kt % S;
+    T* st = smem + s * C::STAGE_ELEMS;
+    mbar_expect_tx(&full[s], kBytes);
+    tma_box(st, mapW, kt * C::BK, w_row0, &full[s]);
+    tma_box(st + C::BM * C::PITCH, mapV, kt * C::BK, v_row0, &full[s]);
+  };
+  if (tid == 0)
+    for (int kt = 0; kt < S && kt < KT; ++kt) issue(kt);
+  const int ty = thread_ty(), tx = thread_tx();
+  for (int kt = 0; kt < KT; ++kt) {
+    const int s = kt % S;
+    const unsigned ph = (unsigned)(kt / S) & 1u;
+    mbar_wait(&full[s], ph);
+    const T* st = smem + s * C::STAGE_ELEMS;
+#pragma unroll C::KKU
+    for (int kk = 0; kk < C::BK; kk += C::VEC)
+      micro_step<C>(acc, st, st + C::BM * C::PITCH, ty, tx, kk);
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+    if (tid == 0 && kt + S < KT) {
+      mbar_wait(&empty[s], ph);  // all warps are done with this slot
+      issue(kt + S);
+    }
+  }
+}
+
 // First column tile of row-tile b in a diagonal task (the tile holding
 // column b*BM + 1: every tile with some i < j); 0 for rectangles.
 __host__ __device__ __forceinline__ int64_t first_col_tile(int64_t b, int64_t bm, int64_t bn,

@@ -644,8 +644,11 @@ struct Run2 : Rank {
   bool layout(psim_out_t* out) {
     setup();
     plan_2way(g->n_pv, g->n_pr, p_v, p_r, n_vp, flags & PSIM_RUN_BALANCE_REFERENCE, &ex, &tasks);
+    // received blocks back to back: consecutive full-width tasks then form one
+    // contiguous V operand (flattened into one grid with TMA staging)
+    char* ring = static_cast<char*>(A.take((int64_t)ex.size() * n_vp * ld * esz));
     for (size_t k = 0; k < ex.size(); ++k) {
-      rblock.push_back(A.take(n_vp * ld * esz));
+      rblock.push_back(ring ? ring + k * n_vp * ld * esz : nullptr);
       rsums.push_back(A.take(n_vp * esz));
     }
     // host input (pinned, or pageable staged through a pinned ring) with a

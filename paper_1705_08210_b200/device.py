@@ -64,15 +64,18 @@ def alloc_block(n_fp: int, n_vp: int, precision: str, device) -> torch.Tensor:
     return torch.empty((n_vp, ld_for(n_fp)), dtype=torch_dtype(precision), device=device)
 
 
-def load_block(problem, grid, coords, device, pinned_cache: dict | None = None) -> Block:
+def load_block(problem, grid, coords, device, pinned_cache: dict | None = None,
+               into: torch.Tensor | None = None) -> Block:
     """The rank's block: generated in HBM for synthetic sources, else copied H2D.
 
     Generic sources are validated on the device (non-finite / negative ->
-    DataError, core.py:239-242)."""
+    DataError, core.py:239-242). ``into``: an (n_vp, ld) slice of a larger
+    allocation to fill (blocks of one field slab back to back, so the
+    kernels can stage consecutive blocks as one operand)."""
     n_fp, n_vp = problem.n_f // grid.n_pf, problem.n_v // grid.n_pv
     f0, _ = field_range(grid, coords.p_f, problem.n_f)
     v0, _ = vector_range(grid, coords.p_v, problem.n_v)
-    data = alloc_block(n_fp, n_vp, problem.precision, device)
+    data = alloc_block(n_fp, n_vp, problem.precision, device) if into is None else into
     ld = data.shape[1]
     code = code_of(problem.precision)
     src = problem.source

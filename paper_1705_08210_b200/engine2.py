@@ -260,9 +260,14 @@ def run_local(problem, grid, balance: str = "split", keep_values: bool = True,
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record()
     blocks = {}
-    for p_v in range(grid.n_pv):
-        for p_f in range(grid.n_pf):
-            blocks[p_f, p_v] = D.load_block(problem, grid, RankCoords(p_f, p_v, 0), dev)
+    for p_f in range(grid.n_pf):
+        # the slabs of one field range back to back in one allocation: a rank's
+        # consecutive off-diagonal tasks then read one contiguous V operand
+        n_fp = problem.n_f // grid.n_pf
+        slab = D.alloc_block(n_fp, n_vp * grid.n_pv, problem.precision, dev)
+        for p_v in range(grid.n_pv):
+            blocks[p_f, p_v] = D.load_block(problem, grid, RankCoords(p_f, p_v, 0), dev,
+                                            into=slab[p_v * n_vp:(p_v + 1) * n_vp])
     sums = {p_v: fold_sums([D.column_sums(blocks[p_f, p_v]) for p_f in range(grid.n_pf)], code)
             for p_v in range(grid.n_pv)}
     acc = D.new_acc(dev)

@@ -489,24 +489,36 @@ def test_streamed_capi_validation():
     t = N.Block2(W=dev.data_ptr(), ldw=32, V=dev.data_ptr(), ldv=32, n_f=20, m=10, n=10,
                  diagonal=1, n_v=10, acc=acc.data_ptr(), s_row=sums.data_ptr())
     s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    # pageable host memory is staged through the pinned ring (accepted);
+    # a device pointer passed as the host block is rejected
     rc = lib.psim_czek2_streamed(N.F64, C.byref(t), pageable.ctypes.data, 20, 4,
                                  ready.data_ptr(), s1.cuda_stream, s2.cuda_stream)
-    assert rc == 1 and b"pinned" in lib.psim_last_error()
+    assert rc == 0, lib.psim_last_error()
+    torch.cuda.synchronize()
+    rc = lib.psim_czek2_streamed(N.F64, C.byref(t), dev.data_ptr(), 32, 4,
+                                 ready.data_ptr(), s1.cuda_stream, s2.cuda_stream)
+    assert rc == 1 and b"device memory" in lib.psim_last_error()
     t.diagonal = 0
     rc = lib.psim_czek2_streamed(N.F64, C.byref(t), pageable.ctypes.data, 20, 4,
                                  ready.data_ptr(), s1.cuda_stream, s2.cuda_stream)
     assert rc == 1
 
 
+@pytest.mark.parametrize("loader", ["tma", "cp.async"])
 @pytest.mark.parametrize("precision", ["double", "single"])
-def test_flattened_offdiagonal_tasks_bitwise_vs_oracle(precision):
+def test_flattened_offdiagonal_tasks_bitwise_vs_oracle(precision, loader, monkeypatch):
     """Blocks wider than a column tile: a rank's off-diagonal circulant tasks
     run as one kCzek2Flat task (columns end to end, tiles straddling two
     blocks; czek2.cu flatten_tasks). n_vp = 500 / 375 / 300 / 250 covers full
     tasks, split half-blocks wider (187) and narrower (125) than BN, which stay
     separate. Identical bits and checksum to the sequential oracle, with and
-    without kept values."""
+    without kept values. With TMA staging (default) only blocks that lie back
+    to back in memory are flattened (one V operand); PSIM_NO_TMA=1 runs the
+    cp.async loader, whose two-pointer tiles flatten any consecutive blocks."""
     from oracle import propsim_np as O
+
+    if loader == "cp.async":
+        monkeypatch.setenv("PSIM_NO_TMA", "1")
 
     P = _api()
     n_f, n_v = 257, 1500
