@@ -16,15 +16,13 @@
 // task's ragged last row tile as a 32-row edge task (czek2_tasks_t).
 #include <cstdlib>
 
-#include <cuda.h>
-#include <cudaTypedefs.h>
-
 #include <cstring>
 #include <mutex>
 #include <thread>
 #include <vector>
 
 #include "minplus.cuh"
+#include "psim_tma.h"
 #include "psim_internal.h"
 
 namespace psim {
@@ -445,46 +443,9 @@ static int64_t plan2(Args2<typename C::T>& a, int64_t row_begin, int64_t row_end
   return blocks;
 }
 
-// Tensor maps for TMA staging (minplus_tile_tma). The encoder comes from the
-// driver through the runtime (no libcuda link); PSIM_NO_TMA=1 keeps the
-// cp.async loader (A/B). A flattened group uses TMA only when its segments
-// lie back to back in memory (one V operand); otherwise the two-pointer
-// cp.async loader runs.
-// TMA staging on unless PSIM_NO_TMA=1 (read per launch, so tests can A/B it).
-static bool tma_enabled() {
-  const char* v = getenv("PSIM_NO_TMA");
-  return !(v && v[0] == '1');
-}
-
-static PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
-    PFN_cuTensorMapEncodeTiled_v12000 f = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&f, cudaEnableDefault, &q) !=
-            cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      f = nullptr;
-    cudaGetLastError();
-    return f;
-  }();
-  return fn;
-}
-
-template <typename T>
-static bool encode_operand(CUtensorMap* map, const T* base, int64_t n_f, int64_t vectors,
-                           int64_t ld, int box_rows, int pitch) {
-  auto enc = tma_encoder();
-  if (!enc || !base || vectors < 1 || n_f < 1 || n_f >= (1ll << 31) || vectors >= (1ll << 31))
-    return false;
-  const cuuint64_t dims[2] = {(cuuint64_t)n_f, (cuuint64_t)vectors};
-  const cuuint64_t strides[1] = {(cuuint64_t)(ld * (int64_t)sizeof(T))};
-  const cuuint32_t box[2] = {(cuuint32_t)pitch, (cuuint32_t)box_rows}, es[2] = {1, 1};
-  return enc(map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-             2, const_cast<T*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
+// Tensor maps for TMA staging (minplus_tile_tma): psim_tma.h. A flattened
+// group uses TMA only when its segments lie back to back in memory (one V
+// operand); otherwise the two-pointer cp.async loader runs.
 template <class C>
 static void setup_tma(Args2<typename C::T>& a, int mode) {
   using T = typename C::T;
