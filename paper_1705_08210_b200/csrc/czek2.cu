@@ -742,13 +742,12 @@ void copy_rows(char* dst, int64_t dst_ld, const char* src, int64_t src_ld, int64
 }
 }  // namespace
 
-static cudaError_t stage_pageable(void* dst_, int64_t ldw, const void* src_, int64_t host_ld,
-                                  int64_t n_f, int64_t n, int64_t chunk, size_t sz,
-                                  unsigned* ready, const unsigned* one, int64_t nflags,
-                                  cudaStream_t copy) {
+// Grow the ring to `need` bytes per slot. Called BEFORE the streamed kernel
+// is launched: cudaFreeHost / cudaHostAlloc synchronize with the device, and a
+// launched kernel waiting for chunks would deadlock against them.
+static cudaError_t prepare_ring(size_t need) {
   PinnedRing& R = ring();
   std::lock_guard<std::mutex> lock(R.mu);
-  const size_t need = (size_t)chunk * ldw * sz;
   cudaError_t e = cudaSuccess;
   if (R.cap < need) {
     for (int k = 0; k < kRing; ++k) {
@@ -763,6 +762,16 @@ static cudaError_t stage_pageable(void* dst_, int64_t ldw, const void* src_, int
     }
     if (e == cudaSuccess) R.cap = need;
   }
+  return e;
+}
+
+static cudaError_t stage_pageable(void* dst_, int64_t ldw, const void* src_, int64_t host_ld,
+                                  int64_t n_f, int64_t n, int64_t chunk, size_t sz,
+                                  unsigned* ready, const unsigned* one, int64_t nflags,
+                                  cudaStream_t copy) {
+  PinnedRing& R = ring();
+  std::lock_guard<std::mutex> lock(R.mu);
+  cudaError_t e = R.cap >= (size_t)chunk * ldw * sz ? cudaSuccess : cudaErrorInvalidValue;
   char* dst = static_cast<char*>(dst_);
   const char* src = static_cast<const char*>(src_);
   const int64_t nchunks = (n + chunk - 1) / chunk;
@@ -809,6 +818,11 @@ cudaError_t czek2_streamed_t(const Czek2Block& t, const void* host, int64_t host
   if (e == cudaSuccess) e = cudaStreamWaitEvent(compute, cleared, 0);
   cudaEventDestroy(cleared);
   if (e != cudaSuccess) return e;
+  cudaPointerAttributes pa{};
+  const bool pinned = cudaPointerGetAttributes(&pa, host) == cudaSuccess &&
+                      pa.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  if (!pinned && (e = prepare_ring((size_t)chunk * t.ldw * sizeof(T))) != cudaSuccess) return e;
   void* abort_flag = nullptr;  // cleared before every streamed launch
   if ((e = cudaGetSymbolAddress(&abort_flag, g_stream_abort)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(abort_flag, 0, sizeof(unsigned), compute)) != cudaSuccess) return e;
@@ -826,10 +840,6 @@ cudaError_t czek2_streamed_t(const Czek2Block& t, const void* host, int64_t host
     return e;
   T* dst = static_cast<T*>(const_cast<void*>(t.W));
   const T* src = static_cast<const T*>(host);
-  cudaPointerAttributes pa{};
-  const bool pinned = cudaPointerGetAttributes(&pa, host) == cudaSuccess &&
-                      pa.type == cudaMemoryTypeHost;
-  cudaGetLastError();
   if (!pinned)  // pageable: staged through a pinned ring, chunk by chunk
     return stage_pageable(dst, t.ldw, src, host_ld, t.n_f, n, chunk, sz, ready, one, nflags, copy);
   for (int64_t c = nchunks - 1; c >= 0; --c) {

@@ -554,7 +554,12 @@ __device__ __forceinline__ void minplus_tile_pivot_tma(const void* mapA, int a_r
     if (kt + 1 < KT) transform(kt + 1);
     mbar_wait(&ready[s], ph);
     const T* st = smem + s * C::STAGE_ELEMS;
-#pragma unroll
+#ifdef PSIM_PIVOT_TMA_KKU
+    constexpr int U = PSIM_PIVOT_TMA_KKU;
+#else
+    constexpr int U = C::KKU;
+#endif
+#pragma unroll U
     for (int kk = 0; kk < C::BK; kk += C::VEC)
       micro_step<C>(acc, st, st + C::BM * C::PITCH, ty, tx, kk);
     __syncwarp();
