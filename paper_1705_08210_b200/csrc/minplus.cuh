@@ -496,7 +496,7 @@ __device__ __forceinline__ void minplus_tile_tma(const void* mapW, int w_row0, c
 // pivot chunk (a third box: PITCH fields of the pivot vector, zero past n_f)
 // and the pivot min A[r][q] <- min(x_j[q], A[r][q]) applied in shared memory
 // (xj_columns, mingemm.py:225-234) by every thread to its share of the stage,
-// one stage ahead of the compute: warps publish the transformed stage on a
+// D stages ahead of the compute: warps publish the transformed stage on a
 // per-stage "ready" mbarrier, so the transform needs no CTA-wide barrier.
 template <class C>
 __device__ __forceinline__ void minplus_tile_pivot_tma(const void* mapA, int a_row0,
@@ -544,14 +544,18 @@ __device__ __forceinline__ void minplus_tile_pivot_tma(const void* mapA, int a_r
     __syncwarp();
     if (lane == 0) mbar_arrive(&ready[s]);
   };
+  // transform D stages ahead of the compute: a warp may then run up to D
+  // stages ahead of the slowest one before it waits on a "ready" barrier (the
+  // stage D ahead was issued S - D iterations earlier, so it has landed)
+  constexpr int D = S >= 4 ? 2 : 1;
   if (tid == 0)
     for (int kt = 0; kt < S && kt < KT; ++kt) issue(kt);
-  if (KT > 0) transform(0);
+  for (int kt = 0; kt < D && kt < KT; ++kt) transform(kt);
   const int ty = thread_ty(), tx = thread_tx();
   for (int kt = 0; kt < KT; ++kt) {
     const int s = kt % S;
     const unsigned ph = (unsigned)(kt / S) & 1u;
-    if (kt + 1 < KT) transform(kt + 1);
+    if (kt + D < KT) transform(kt + D);
     mbar_wait(&ready[s], ph);
     const T* st = smem + s * C::STAGE_ELEMS;
 #ifdef PSIM_PIVOT_TMA_KKU
