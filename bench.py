@@ -484,7 +484,8 @@ def sampled_parity(runner, prob, bits, world, dev) -> dict:
     triple recompute) and compared bit for bit with the values the kernels
     wrote. 2-way: per value piece of this rank, a grid of sampled rows x
     sampled columns (so ~10^4 pairs need only a few hundred generated
-    columns); 3-way: 300 triples of the last pivot chunk. Mismatches and
+    columns); 3-way: ~10^4 triples (16 pivots x a 25 x 25 grid) of the
+    last pivot chunk. Mismatches and
     sample counts are summed over ranks."""
     import torch
 
@@ -542,24 +543,28 @@ def sampled_parity(runner, prob, bits, world, dev) -> dict:
             offs[j] = off
             off += max(0, min(box.i1, j) - box.i0) * max(0, box.k1 - max(box.k0, j + 1))
         assert off == box_count(box)
-        triples = set()
-        while len(triples) < 300:
-            j = int(rng.integers(max(box.j0, 1), min(box.j1, n_v - 1)))
-            i = int(rng.integers(0, j))
-            k = int(rng.integers(j + 1, n_v))
-            triples.add((i, j, k))
-        triples = sorted(triples)
-        pos = [offs[j] + i * (n_v - j - 1) + (k - j - 1) for i, j, k in triples]
-        got = D.to_host(runner.buf[torch.as_tensor(pos, device=runner.buf.device)])
-        cols = sorted({c for t in triples for c in t})
-        at = {c: x for x, c in enumerate(cols)}
-        V = O.random_exact_cols(SEED, n_f, n_v, bits, cols, dt)
-        want = O.triple_values_sampled(V, [tuple(at[c] for c in t) for t in triples])
-        mismatches = int((got.view(np.uint8).reshape(len(got), -1)
-                          != want.view(np.uint8).reshape(len(want), -1)).any(axis=1).sum())
-        sampled = len(got)
-        how = ("300 triples of the last pivot chunk, recomputed from their three columns by "
-               "oracle.propsim_np.triple_values_sampled")
+        # 16 pivots of the chunk x (25 sampled rows x 25 sampled columns) each:
+        # ~10^4 triples, recomputed as grids (oracle.triple_values_grid)
+        js = [j for j in range(box.j0, box.j1)
+              if min(box.i1, j) > box.i0 and box.k1 > max(box.k0, j + 1)]
+        js = sorted(set(int(x) for x in rng.choice(js, size=min(16, len(js)), replace=False)))
+        for j in js:
+            klo = max(box.k0, j + 1)
+            ih, kh = min(box.i1, j), box.k1
+            rows = np.unique(np.concatenate([rng.integers(box.i0, ih, size=23), [box.i0, ih - 1]]))
+            cols = np.unique(np.concatenate([rng.integers(klo, kh, size=23), [klo, kh - 1]]))
+            VI = O.random_exact_cols(SEED, n_f, n_v, bits, rows, dt)
+            VK = O.random_exact_cols(SEED, n_f, n_v, bits, cols, dt)
+            xj = O.random_exact_cols(SEED, n_f, n_v, bits, [j], dt)[:, 0]
+            want = O.triple_values_grid(VI, xj, VK).ravel()
+            ii, kk = np.meshgrid(rows, cols, indexing="ij")
+            pos = offs[j] + (ii - box.i0) * (box.k1 - klo) + (kk - klo)
+            got = D.to_host(runner.buf[torch.as_tensor(pos.ravel(), device=runner.buf.device)])
+            mismatches += int((got.view(np.uint8).reshape(len(got), -1)
+                               != want.view(np.uint8).reshape(len(want), -1)).any(axis=1).sum())
+            sampled += len(got)
+        how = (f"{len(js)} pivots of the last pivot chunk x (sampled rows x sampled columns), "
+               "recomputed from their columns by oracle.propsim_np.triple_values_grid")
     else:
         return {"sampled": 0, "mismatches": 0, "note": "values not retained by this harness"}
     if world > 1:

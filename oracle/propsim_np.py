@@ -312,6 +312,34 @@ def pair_values_grid(VR, VC, n_pf: int = 1):
     return out
 
 
+def triple_values_grid(VI, xj, VK, n_pf: int = 1):
+    """3-way values of every (i, j, k) with one pivot column xj (n_f,), rows
+    VI (n_f, a) and columns VK (n_f, b), recomputed from those columns only:
+    pair_numerators / triple_min_numerators (mingemm.py:237-260), column_sums
+    and metric3_value (metrics3.py:38-44) with the canonical roles i < j < k
+    (the caller passes i < j < k). Returns an (a, b) array."""
+    VI = np.asarray(VI)
+    dt = VI.dtype.type
+    xj = np.asarray(xj, dtype=VI.dtype)[:, None]
+    VK = np.asarray(VK, dtype=VI.dtype)
+    si, sk = _seq_sum_cols(VI, n_pf), _seq_sum_cols(VK, n_pf)
+    sj = _seq_sum_cols(xj, n_pf)[0]
+    nij = _seq_sum_cols(np.where(VI < xj, VI, xj), n_pf)          # (a,)
+    njk = _seq_sum_cols(np.where(xj < VK, xj, VK), n_pf)          # (b,)
+    ab = np.where(VI < xj, VI, xj)                                # min(v_i, x_j)
+    out = np.empty((VI.shape[1], VK.shape[1]), dtype=VI.dtype)
+    for r in range(VI.shape[1]):
+        a, m = VI[:, r:r + 1], ab[:, r:r + 1]
+        nik = _seq_sum_cols(np.where(a < VK, a, VK), n_pf)
+        n3p = _seq_sum_cols(np.where(m < VK, m, VK), n_pf)
+        n3 = ((nij[r] + nik) + njk) - n3p
+        d = (si[r] + sj) + sk
+        with np.errstate(divide="ignore", invalid="ignore"):
+            v = (dt(1.5) * n3) / d
+        out[r] = np.where(d == 0, dt(0), v)
+    return out
+
+
 def uniform_cols(seed: int, n_f: int, n_v: int, cols, dtype=np.float64):
     """Selected global columns of the uniform matrix."""
     q = np.arange(n_f, dtype=np.uint64)[:, None]

@@ -57,3 +57,28 @@ def test_oracle_whole_run_checksum(idx):
     _, cks, deg = c_oracle.czek2(V)
     assert cks == c["checksum"]
     assert deg == c["degenerate"]
+
+
+@pytest.mark.parametrize("idx", [i for i, c in enumerate(CASES) if c["arity"] == 3])
+def test_triple_values_grid_matches_reference_samples(idx):
+    """The grid recompute bench.py uses for its ~10^4-triple parity check of
+    cfg4 (oracle.triple_values_grid) reproduces the reference's sampled 3-way
+    values: every sampled triple of the golden case, as a 1 x 1 grid around
+    its pivot, and the whole grid equals the per-triple recompute."""
+    c = CASES[idx]
+    tuples = _tuples(3, c["n_v"])
+    n_pf = c["grid"]["n_pf"]
+    for p, want in list(c["sample"].items())[:20]:
+        i, j, k = tuples[int(p)]
+        V = _cols(c, [i, j, k])
+        got = O.triple_values_grid(V[:, :1], V[:, 1], V[:, 2:], n_pf)
+        assert format(int(O.value_bits(got.ravel())[0]), "x") == want, p
+    # a whole grid vs the per-triple restatement
+    j = c["n_v"] // 2
+    rows, cols = list(range(0, j, 7)), list(range(j + 1, c["n_v"], 5))
+    V = _cols(c, rows + [j] + cols)
+    a = len(rows)
+    grid = O.triple_values_grid(V[:, :a], V[:, a], V[:, a + 1:], n_pf)
+    per = O.triple_values_sampled(V, [(r, a, a + 1 + q) for r in range(a)
+                                      for q in range(len(cols))], n_pf)
+    assert (O.value_bits(grid.ravel()) == O.value_bits(per)).all()
