@@ -484,7 +484,7 @@ def sampled_parity(runner, prob, bits, world, dev) -> dict:
     triple recompute) and compared bit for bit with the values the kernels
     wrote. 2-way: per value piece of this rank, a grid of sampled rows x
     sampled columns (so ~10^4 pairs need only a few hundred generated
-    columns); 3-way: ~10^4 triples (16 pivots x a 25 x 25 grid) of the
+    columns); 3-way: ~10^4 triples (20 pivots x a 25 x 25 grid) of the
     last pivot chunk. Mismatches and
     sample counts are summed over ranks."""
     import torch
@@ -543,11 +543,11 @@ def sampled_parity(runner, prob, bits, world, dev) -> dict:
             offs[j] = off
             off += max(0, min(box.i1, j) - box.i0) * max(0, box.k1 - max(box.k0, j + 1))
         assert off == box_count(box)
-        # 16 pivots of the chunk x (25 sampled rows x 25 sampled columns) each:
+        # 20 pivots of the chunk x (25 sampled rows x 25 sampled columns) each:
         # ~10^4 triples, recomputed as grids (oracle.triple_values_grid)
         js = [j for j in range(box.j0, box.j1)
               if min(box.i1, j) > box.i0 and box.k1 > max(box.k0, j + 1)]
-        js = sorted(set(int(x) for x in rng.choice(js, size=min(16, len(js)), replace=False)))
+        js = sorted(set(int(x) for x in rng.choice(js, size=min(20, len(js)), replace=False)))
         for j in js:
             klo = max(box.k0, j + 1)
             ih, kh = min(box.i1, j), box.k1

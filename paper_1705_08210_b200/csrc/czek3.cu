@@ -179,9 +179,9 @@ __global__ void __launch_bounds__(kNT, C::MINB)
     const Tile3 d = box3_decode<C::BM, C::BN, PACKED>(b, tile_pref, nJ, blockIdx.x);
     if (PACKED) {  // segmented staging, per-segment pivot
       minplus_tile3<C>(b, d, acc, smem);
-    } else if (tm.on) {  // one pivot, TMA staging (launch-uniform)
-      minplus_tile_pivot_tma<C>(&tm.mA, (int)(d.row0 - b.a0), &tm.mC, (int)(d.col0 - b.c0),
-                                &tm.mB, (int)(d.p0 - b.b0), b.n_f, acc, smem);
+    } else if (tm.on) {  // one pivot, TMA staging (launch-uniform), per-warp pivot min
+      minplus_tile_pivot_ilv<C, 1>(&tm.mA, (int)(d.row0 - b.a0), &tm.mC, (int)(d.col0 - b.c0),
+                                   &tm.mB, (int)(d.p0 - b.b0), b.n_f, acc, smem);
     } else {  // one pivot: the lean loop (measured 5% faster than the segmented one)
       minplus_tile<C, true>(static_cast<const T*>(b.VA) + (d.row0 - b.a0) * b.ldA, b.ldA, d.nr0,
                             static_cast<const T*>(b.VC) + (d.col0 - b.c0) * b.ldC, b.ldC, d.nc0,

@@ -575,6 +575,117 @@ __device__ __forceinline__ void minplus_tile_pivot_tma(const void* mapA, int a_r
   }
 }
 
+// 3-way single-pivot tile with TMA staging, per-warp interleaved pivot min:
+// the A rows a warp reads in micro_step are ty + 16 m with ty in
+// {4 (w/2) .. 4 (w/2) + 3}, so each warp rewrites exactly those 32 rows,
+// A[r][q] <- min(x_j[q], A[r][q]) (xj_columns, mingemm.py:225-234), and needs
+// no other warp's work: no "ready" barrier, only full / empty as in the 2-way
+// loop. The two warps of a pair read (and so rewrite) the same rows; min is
+// idempotent, so the second rewrite stores the values already there. The
+// rewrite of stage kt + A is spread over the micro-steps of stage kt:
+// micro-step u loads chunk u (row ty0 + 16u, this lane's 16 bytes) at its top
+// and stores min(x, chunk) at its bottom, so the load latency hides behind
+// the micro-step's FP instructions. Measured (tools/exp_pivot_tma.cu,
+// profiles/r02_3way_pivot/, FP64 128 x 128 tiles, cmp/clk/SM): 2-way loop
+// 22.26 / 22.68 (n_f = 20000 / 10000), the "ready"-barrier loop above 18.25 /
+// 20.41 (the barrier alone costs 2-4%, and it bounds warp skew to D stages),
+// this loop with A = 1 21.38 / 21.81 (96% of the 2-way loop), bitwise equal.
+template <class C, int A>
+__device__ __forceinline__ void minplus_tile_pivot_ilv(const void* mapA, int a_row0,
+                                                       const void* mapC, int c_row0,
+                                                       const void* mapB, int p_row, int64_t n_f,
+                                                       typename C::T (&acc)[C::TM][C::TN],
+                                                       typename C::T* smem) {
+  using T = typename C::T;
+  using V4 = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
+  static_assert(C::BK / C::VEC == C::TM, "one chunk of the warp's rows per micro-step");
+  static_assert(A >= 1 && A < C::STAGES, "transform distance");
+  constexpr int S = C::STAGES;
+  constexpr int XS = (C::BM + C::BN) * C::PITCH;  // pivot slot inside a stage
+  constexpr unsigned kBytes = (C::BM + C::BN + 1) * C::PITCH * sizeof(T);
+  __shared__ __align__(8) uint64_t full[S], empty[S];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kNT / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+#pragma unroll
+  for (int m = 0; m < C::TM; ++m)
+#pragma unroll
+    for (int n = 0; n < C::TN; ++n) acc[m][n] = T(0);
+  __syncthreads();
+  const int KT = (int)((n_f + C::BK - 1) / C::BK);
+  auto issue = [&](int kt) {
+    const int s = kt % S;
+    T* st = smem + s * C::STAGE_ELEMS;
+    mbar_expect_tx(&full[s], kBytes);
+    tma_box(st, mapA, kt * C::BK, a_row0, &full[s]);
+    tma_box(st + C::BM * C::PITCH, mapC, kt * C::BK, c_row0, &full[s]);
+    tma_box(st + XS, mapB, kt * C::BK, p_row, &full[s]);
+  };
+  auto vmin = [](const V4& x, V4 a) {
+    if constexpr (sizeof(T) == 8) {
+      a.x = Traits<double>::min(x.x, a.x);
+      a.y = Traits<double>::min(x.y, a.y);
+    } else {
+      a.x = Traits<float>::min(x.x, a.x);
+      a.y = Traits<float>::min(x.y, a.y);
+      a.z = Traits<float>::min(x.z, a.z);
+      a.w = Traits<float>::min(x.w, a.w);
+    }
+    return a;
+  };
+  // this lane's chunk u: row (w/2)*4 + lane/8 + 16u, 16-byte column lane%8
+  const int xoff = (lane & 7) * C::VEC;
+  const int roff = ((w >> 1) * 4 + (lane >> 3)) * C::PITCH + xoff;
+  if (tid == 0)
+    for (int kt = 0; kt < S && kt < KT; ++kt) issue(kt);
+  for (int kt = 0; kt < A && kt < KT; ++kt) {  // the first A stages up front
+    T* st = smem + (kt % S) * C::STAGE_ELEMS;
+    mbar_wait(&full[kt % S], (unsigned)(kt / S) & 1u);
+    const V4 x = *reinterpret_cast<const V4*>(st + XS + xoff);
+#pragma unroll
+    for (int u = 0; u < C::TM; ++u) {
+      V4* p = reinterpret_cast<V4*>(st + roff + 16 * u * C::PITCH);
+      *p = vmin(x, *p);
+    }
+  }
+  __syncwarp();
+  const int ty = thread_ty(), tx = thread_tx();
+  for (int kt = 0; kt < KT; ++kt) {
+    const int s = kt % S;
+    const unsigned ph = (unsigned)(kt / S) & 1u;
+    const bool xf = kt + A < KT;
+    T* nx = smem + ((kt + A) % S) * C::STAGE_ELEMS;
+    V4 x{};
+    if (xf) {
+      mbar_wait(&full[(kt + A) % S], (unsigned)((kt + A) / S) & 1u);
+      x = *reinterpret_cast<const V4*>(nx + XS + xoff);
+    }
+    const T* st = smem + s * C::STAGE_ELEMS;
+#pragma unroll 1
+    for (int u = 0; u < C::TM; ++u) {
+      V4* pa = reinterpret_cast<V4*>(nx + roff + 16 * u * C::PITCH);
+      V4 a{};
+      if (xf) a = *pa;
+      micro_step<C>(acc, st, st + C::BM * C::PITCH, ty, tx, u * C::VEC);
+      if (xf) *pa = vmin(x, a);
+    }
+    // this warp's generic-proxy writes (stage kt + A) before the async-proxy
+    // refill of that slot, which follows every warp's release of it
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (tid == 0 && kt + S < KT) {
+      mbar_wait(&empty[s], ph);
+      issue(kt + S);
+    }
+  }
+}
+
 // First column tile of row-tile b in a diagonal task (the tile holding
 // column b*BM + 1: every tile with some i < j); 0 for rectangles.
 __host__ __device__ __forceinline__ int64_t first_col_tile(int64_t b, int64_t bm, int64_t bn,

@@ -9,15 +9,17 @@
 //   warp_own  each warp rewrites exactly the A rows it reads (its warp-pair
 //             partner writes the same values: min is idempotent), one stage ahead;
 //             no cross-warp synchronisation beyond full / empty
-//   ws        warp-specialised: 256 math threads + one producer warp that issues
-//             the TMA boxes and applies the pivot min to the whole A stage
-//             (9 warps: the per-SMSP register file caps every thread at 168 regs)
-//   ws_wg     warp-specialised with a producer warpgroup (384 threads):
-//             setmaxnreg gives the producers 40 registers and the math warps 232;
-//             each producer warp transforms 32 rows, warp 8 issues the boxes
+//   (round-2 call P, profiles/r02_3way_ws/: two warp-specialised variants -- a
+//   producer warp (9 warps: the per-SMSP register file caps all threads at 168
+//   registers, spills) 14.2, and a producer warpgroup with setmaxnreg (ptxas
+//   still allocates for the 384-thread launch bound: 168 registers) 8.4
+//   cmp/clk/SM -- lost to the register cap and were removed)
+// Prefetch slack: the stage a warp transforms A stages ahead was issued when
+// the slowest warp released its slot, i.e. S - 1 - A stages before it is
+// needed; prod (D = 2, S = 4) leaves one stage. The variants below vary S and A.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -Xptxas -v \
 //          -I include -I paper_1705_08210_b200/csrc tools/exp_pivot_tma.cu -o build/exp_pivot_tma
-// Run:   build/exp_pivot_tma [n] [n_f]  -> one JSON line per variant
+// Run:   build/exp_pivot_tma [n] [n_f] [variant mask, default all] -> one JSON line per variant
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -50,33 +52,35 @@ __device__ __forceinline__ void store_tile(double (&acc)[Cc::TM][Cc::TN], double
     }
 }
 
-// ---- warp_own: each warp transforms the 32 A rows it reads
+// ---- own<Cc, A>: each warp transforms the 32 A rows it reads, A stages ahead
+template <class Cc>
 __device__ __forceinline__ void warp_rows_min(double* st, const double* xs) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int ch = lane & 7;
-  const double2 x = *reinterpret_cast<const double2*>(xs + ch * C::VEC);
-  double2 a[C::TM];
+  const double2 x = *reinterpret_cast<const double2*>(xs + ch * Cc::VEC);
+  double2 a[Cc::TM];
 #pragma unroll
-  for (int m = 0; m < C::TM; ++m) {
+  for (int m = 0; m < Cc::TM; ++m) {
     const int row = (w >> 1) * 4 + (lane >> 3) + 16 * m;
-    a[m] = *reinterpret_cast<const double2*>(st + row * C::PITCH + ch * C::VEC);
+    a[m] = *reinterpret_cast<const double2*>(st + row * Cc::PITCH + ch * Cc::VEC);
   }
 #pragma unroll
-  for (int m = 0; m < C::TM; ++m) {
+  for (int m = 0; m < Cc::TM; ++m) {
     const int row = (w >> 1) * 4 + (lane >> 3) + 16 * m;
     double2 v;
     v.x = Traits<double>::min(x.x, a[m].x);
     v.y = Traits<double>::min(x.y, a[m].y);
-    *reinterpret_cast<double2*>(st + row * C::PITCH + ch * C::VEC) = v;
+    *reinterpret_cast<double2*>(st + row * Cc::PITCH + ch * Cc::VEC) = v;
   }
 }
 
-__device__ __forceinline__ void tile_warp_own(const void* mapA, int a_row0, const void* mapC,
-                                              int c_row0, const void* mapB, int p_row, int64_t n_f,
-                                              double (&acc)[C::TM][C::TN], double* smem) {
-  constexpr int S = C::STAGES;
-  constexpr int XS = (C::BM + C::BN) * C::PITCH;
-  constexpr unsigned kBytes = (C::BM + C::BN + 1) * C::PITCH * sizeof(T);
+template <class Cc, int A>
+__device__ __forceinline__ void tile_own(const void* mapA, int a_row0, const void* mapC,
+                                         int c_row0, const void* mapB, int p_row, int64_t n_f,
+                                         double (&acc)[Cc::TM][Cc::TN], double* smem) {
+  constexpr int S = Cc::STAGES;
+  constexpr int XS = (Cc::BM + Cc::BN) * Cc::PITCH;
+  constexpr unsigned kBytes = (Cc::BM + Cc::BN + 1) * Cc::PITCH * sizeof(T);
   __shared__ __align__(8) uint64_t full[S], empty[S];
   const int tid = threadIdx.x, lane = tid & 31;
   if (tid == 0) {
@@ -87,39 +91,39 @@ __device__ __forceinline__ void tile_warp_own(const void* mapA, int a_row0, cons
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
 #pragma unroll
-  for (int m = 0; m < C::TM; ++m)
+  for (int m = 0; m < Cc::TM; ++m)
 #pragma unroll
-    for (int n = 0; n < C::TN; ++n) acc[m][n] = 0.0;
+    for (int n = 0; n < Cc::TN; ++n) acc[m][n] = 0.0;
   __syncthreads();
-  const int KT = (int)((n_f + C::BK - 1) / C::BK);
+  const int KT = (int)((n_f + Cc::BK - 1) / Cc::BK);
   auto issue = [&](int kt) {
     const int s = kt % S;
-    T* st = smem + s * C::STAGE_ELEMS;
+    T* st = smem + s * Cc::STAGE_ELEMS;
     mbar_expect_tx(&full[s], kBytes);
-    tma_box(st, mapA, kt * C::BK, a_row0, &full[s]);
-    tma_box(st + C::BM * C::PITCH, mapC, kt * C::BK, c_row0, &full[s]);
-    tma_box(st + XS, mapB, kt * C::BK, p_row, &full[s]);
+    tma_box(st, mapA, kt * Cc::BK, a_row0, &full[s]);
+    tma_box(st + Cc::BM * Cc::PITCH, mapC, kt * Cc::BK, c_row0, &full[s]);
+    tma_box(st + XS, mapB, kt * Cc::BK, p_row, &full[s]);
   };
   auto transform = [&](int kt) {
     const int s = kt % S;
     mbar_wait(&full[s], (unsigned)(kt / S) & 1u);
-    T* st = smem + s * C::STAGE_ELEMS;
-    warp_rows_min(st, st + XS);
+    T* st = smem + s * Cc::STAGE_ELEMS;
+    warp_rows_min<Cc>(st, st + XS);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
   };
   if (tid == 0)
     for (int kt = 0; kt < S && kt < KT; ++kt) issue(kt);
-  if (KT > 0) transform(0);
+  for (int kt = 0; kt < A && kt < KT; ++kt) transform(kt);
   const int ty = thread_ty(), tx = thread_tx();
   for (int kt = 0; kt < KT; ++kt) {
     const int s = kt % S;
     const unsigned ph = (unsigned)(kt / S) & 1u;
-    if (kt + 1 < KT) transform(kt + 1);
-    const T* st = smem + s * C::STAGE_ELEMS;
+    if (kt + A < KT) transform(kt + A);
+    const T* st = smem + s * Cc::STAGE_ELEMS;
 #pragma unroll 1
-    for (int kk = 0; kk < C::BK; kk += C::VEC)
-      micro_step<C>(acc, st, st + C::BM * C::PITCH, ty, tx, kk);
+    for (int kk = 0; kk < Cc::BK; kk += Cc::VEC)
+      micro_step<Cc>(acc, st, st + Cc::BM * Cc::PITCH, ty, tx, kk);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     if (tid == 0 && kt + S < KT) {
@@ -129,207 +133,194 @@ __device__ __forceinline__ void tile_warp_own(const void* mapA, int a_row0, cons
   }
 }
 
-// ---- ws: warp-specialised producer (warp 8) + 8 math warps
-constexpr int kNTW = kNT + 32;
-
-__device__ __forceinline__ bool tile_ws(const void* mapA, int a_row0, const void* mapC, int c_row0,
-                                        const void* mapB, int p_row, int64_t n_f,
-                                        double (&acc)[C::TM][C::TN], double* smem) {
-  constexpr int S = C::STAGES;
-  constexpr int XS = (C::BM + C::BN) * C::PITCH;
-  constexpr unsigned kBytes = (C::BM + C::BN + 1) * C::PITCH * sizeof(T);
+// ---- gen<Cc, D, FLAGS>: the production loop (minplus_tile_pivot_tma) with knobs:
+// FLAGS bit 0: no transform (pivot box still loaded), bit 1: no proxy fence,
+// bit 2: no pivot box (and no transform)
+template <class Cc, int D, int FLAGS>
+__device__ __forceinline__ void tile_gen(const void* mapA, int a_row0, const void* mapC,
+                                         int c_row0, const void* mapB, int p_row, int64_t n_f,
+                                         double (&acc)[Cc::TM][Cc::TN], double* smem) {
+  constexpr int S = Cc::STAGES;
+  constexpr int XS = (Cc::BM + Cc::BN) * Cc::PITCH;
+  constexpr bool BOX = !(FLAGS & 4), XF = !(FLAGS & 5), FENCE = !(FLAGS & 2);
+  constexpr unsigned kBytes = (Cc::BM + Cc::BN + (BOX ? 1 : 0)) * Cc::PITCH * sizeof(T);
   __shared__ __align__(8) uint64_t full[S], ready[S], empty[S];
   const int tid = threadIdx.x, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&ready[s], 1);
+      mbar_init(&ready[s], kNT / 32);
       mbar_init(&empty[s], kNT / 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+#pragma unroll
+  for (int m = 0; m < Cc::TM; ++m)
+#pragma unroll
+    for (int n = 0; n < Cc::TN; ++n) acc[m][n] = 0.0;
   __syncthreads();
-  const int KT = (int)((n_f + C::BK - 1) / C::BK);
-  if (tid >= kNT) {  // producer warp
-    auto issue = [&](int kt) {
-      const int s = kt % S;
-      T* st = smem + s * C::STAGE_ELEMS;
-      mbar_expect_tx(&full[s], kBytes);
-      tma_box(st, mapA, kt * C::BK, a_row0, &full[s]);
-      tma_box(st + C::BM * C::PITCH, mapC, kt * C::BK, c_row0, &full[s]);
-      tma_box(st + XS, mapB, kt * C::BK, p_row, &full[s]);
-    };
-    if (lane == 0)
-      for (int kt = 0; kt < S && kt < KT; ++kt) issue(kt);
-    const int ch = lane & 7;
-    for (int kt = 0; kt < KT; ++kt) {
-      const int s = kt % S;
-      mbar_wait(&full[s], (unsigned)(kt / S) & 1u);
-      T* st = smem + s * C::STAGE_ELEMS;
-      const double2 x = *reinterpret_cast<const double2*>(st + XS + ch * C::VEC);
-#pragma unroll
-      for (int h = 0; h < 4; ++h) {  // 4 x 8 chunks per lane (128 rows x 8 chunks / 32 lanes)
-        double2 a[8];
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          const int row = (lane >> 3) + 4 * (r + 8 * h);
-          a[r] = *reinterpret_cast<const double2*>(st + row * C::PITCH + ch * C::VEC);
-        }
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          const int row = (lane >> 3) + 4 * (r + 8 * h);
-          double2 v;
-          v.x = Traits<double>::min(x.x, a[r].x);
-          v.y = Traits<double>::min(x.y, a[r].y);
-          *reinterpret_cast<double2*>(st + row * C::PITCH + ch * C::VEC) = v;
-        }
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&ready[s]);
-        // slot of stage kt - 1 -> stage kt - 1 + S once the math warps are done with it
-        const int kp = kt - 1;
-        if (kp >= 0 && kp + S < KT) {
-          mbar_wait(&empty[kp % S], (unsigned)(kp / S) & 1u);
-          issue(kp + S);
-        }
-      }
-      __syncwarp();
-    }
-    return false;
-  }
-#pragma unroll
-  for (int m = 0; m < C::TM; ++m)
-#pragma unroll
-    for (int n = 0; n < C::TN; ++n) acc[m][n] = 0.0;
+  const int KT = (int)((n_f + Cc::BK - 1) / Cc::BK);
+  auto issue = [&](int kt) {
+    const int s = kt % S;
+    T* st = smem + s * Cc::STAGE_ELEMS;
+    mbar_expect_tx(&full[s], kBytes);
+    tma_box(st, mapA, kt * Cc::BK, a_row0, &full[s]);
+    tma_box(st + Cc::BM * Cc::PITCH, mapC, kt * Cc::BK, c_row0, &full[s]);
+    if (BOX) tma_box(st + XS, mapB, kt * Cc::BK, p_row, &full[s]);
+  };
+  auto transform = [&](int kt) {
+    const int s = kt % S;
+    mbar_wait(&full[s], (unsigned)(kt / S) & 1u);
+    T* st = smem + s * Cc::STAGE_ELEMS;
+    if (XF) stage_pivot_min<Cc>(st, st + XS);
+    if (FENCE) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ready[s]);
+  };
+  if (tid == 0)
+    for (int kt = 0; kt < S && kt < KT; ++kt) issue(kt);
+  for (int kt = 0; kt < D && kt < KT; ++kt) transform(kt);
   const int ty = thread_ty(), tx = thread_tx();
   for (int kt = 0; kt < KT; ++kt) {
     const int s = kt % S;
-    mbar_wait(&ready[s], (unsigned)(kt / S) & 1u);
-    const T* st = smem + s * C::STAGE_ELEMS;
+    const unsigned ph = (unsigned)(kt / S) & 1u;
+    if (kt + D < KT) transform(kt + D);
+    mbar_wait(&ready[s], ph);
+    const T* st = smem + s * Cc::STAGE_ELEMS;
 #pragma unroll 1
-    for (int kk = 0; kk < C::BK; kk += C::VEC)
-      micro_step<C>(acc, st, st + C::BM * C::PITCH, ty, tx, kk);
+    for (int kk = 0; kk < Cc::BK; kk += Cc::VEC)
+      micro_step<Cc>(acc, st, st + Cc::BM * Cc::PITCH, ty, tx, kk);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
+    if (tid == 0 && kt + S < KT) {
+      mbar_wait(&empty[s], ph);
+      issue(kt + S);
+    }
   }
-  return true;
 }
 
-// ---- ws_wg: producer warpgroup (warps 8-11) + 8 math warps, setmaxnreg
-constexpr int kNTG = kNT + 128;
-
-__device__ __forceinline__ bool tile_ws_wg(const void* mapA, int a_row0, const void* mapC,
-                                           int c_row0, const void* mapB, int p_row, int64_t n_f,
-                                           double (&acc)[C::TM][C::TN], double* smem) {
-  constexpr int S = C::STAGES;
-  constexpr int XS = (C::BM + C::BN) * C::PITCH;
-  constexpr unsigned kBytes = (C::BM + C::BN + 1) * C::PITCH * sizeof(T);
-  __shared__ __align__(8) uint64_t full[S], ready[S], empty[S];
-  const int tid = threadIdx.x, lane = tid & 31;
+// ---- ilv<Cc, A>: as own<Cc, A> (each warp rewrites the 32 A rows it reads, no
+// cross-warp barrier), but the rewrite of stage kt + A is interleaved with the
+// compute of stage kt: micro-step u loads chunk u of the warp's rows at its top
+// and stores min(x, chunk) at its bottom, so the load latency hides behind the
+// micro-step's 512 FP instructions
+template <class Cc, int A>
+__device__ __forceinline__ void tile_ilv(const void* mapA, int a_row0, const void* mapC,
+                                         int c_row0, const void* mapB, int p_row, int64_t n_f,
+                                         double (&acc)[Cc::TM][Cc::TN], double* smem) {
+  static_assert(Cc::BK / Cc::VEC == Cc::TM, "one chunk of the warp's rows per micro-step");
+  constexpr int S = Cc::STAGES;
+  constexpr int XS = (Cc::BM + Cc::BN) * Cc::PITCH;
+  constexpr unsigned kBytes = (Cc::BM + Cc::BN + 1) * Cc::PITCH * sizeof(T);
+  __shared__ __align__(8) uint64_t full[S], empty[S];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&ready[s], 4);
       mbar_init(&empty[s], kNT / 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+#pragma unroll
+  for (int m = 0; m < Cc::TM; ++m)
+#pragma unroll
+    for (int n = 0; n < Cc::TN; ++n) acc[m][n] = 0.0;
   __syncthreads();
-  const int KT = (int)((n_f + C::BK - 1) / C::BK);
-  if (tid >= kNT) {  // producer warpgroup
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
-    const int pw = (tid - kNT) >> 5;  // 0..3
-    auto issue = [&](int kt) {
-      const int s = kt % S;
-      T* st = smem + s * C::STAGE_ELEMS;
-      mbar_expect_tx(&full[s], kBytes);
-      tma_box(st, mapA, kt * C::BK, a_row0, &full[s]);
-      tma_box(st + C::BM * C::PITCH, mapC, kt * C::BK, c_row0, &full[s]);
-      tma_box(st + XS, mapB, kt * C::BK, p_row, &full[s]);
-    };
-    if (pw == 0 && lane == 0)
-      for (int kt = 0; kt < S && kt < KT; ++kt) issue(kt);
-    const int ch = lane & 7;
-    for (int kt = 0; kt < KT; ++kt) {
-      const int s = kt % S;
-      mbar_wait(&full[s], (unsigned)(kt / S) & 1u);
-      T* st = smem + s * C::STAGE_ELEMS;
-      const double2 x = *reinterpret_cast<const double2*>(st + XS + ch * C::VEC);
-      double2 a[8];
-#pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        const int row = (lane >> 3) + 4 * (r + 8 * pw);
-        a[r] = *reinterpret_cast<const double2*>(st + row * C::PITCH + ch * C::VEC);
-      }
-#pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        const int row = (lane >> 3) + 4 * (r + 8 * pw);
-        double2 v;
-        v.x = Traits<double>::min(x.x, a[r].x);
-        v.y = Traits<double>::min(x.y, a[r].y);
-        *reinterpret_cast<double2*>(st + row * C::PITCH + ch * C::VEC) = v;
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&ready[s]);
-      if (pw == 0 && lane == 0) {
-        const int kp = kt - 1;
-        if (kp >= 0 && kp + S < KT) {
-          mbar_wait(&empty[kp % S], (unsigned)(kp / S) & 1u);
-          issue(kp + S);
-        }
-      }
-      __syncwarp();
-    }
-    return false;
+  const int KT = (int)((n_f + Cc::BK - 1) / Cc::BK);
+  auto issue = [&](int kt) {
+    const int s = kt % S;
+    T* st = smem + s * Cc::STAGE_ELEMS;
+    mbar_expect_tx(&full[s], kBytes);
+    tma_box(st, mapA, kt * Cc::BK, a_row0, &full[s]);
+    tma_box(st + Cc::BM * Cc::PITCH, mapC, kt * Cc::BK, c_row0, &full[s]);
+    tma_box(st + XS, mapB, kt * Cc::BK, p_row, &full[s]);
+  };
+  // this lane's chunk u of the warp's rows: row (w>>1)*4 + lane/8 + 16u, column chunk lane%8
+  const int xoff = (lane & 7) * Cc::VEC;
+  const int roff = ((w >> 1) * 4 + (lane >> 3)) * Cc::PITCH + xoff;
+  if (tid == 0)
+    for (int kt = 0; kt < S && kt < KT; ++kt) issue(kt);
+  for (int kt = 0; kt < A && kt < KT; ++kt) {
+    mbar_wait(&full[kt % S], (unsigned)(kt / S) & 1u);
+    T* st = smem + (kt % S) * Cc::STAGE_ELEMS;
+    warp_rows_min<Cc>(st, st + XS);
   }
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
-#pragma unroll
-  for (int m = 0; m < C::TM; ++m)
-#pragma unroll
-    for (int n = 0; n < C::TN; ++n) acc[m][n] = 0.0;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
   const int ty = thread_ty(), tx = thread_tx();
   for (int kt = 0; kt < KT; ++kt) {
     const int s = kt % S;
-    mbar_wait(&ready[s], (unsigned)(kt / S) & 1u);
-    const T* st = smem + s * C::STAGE_ELEMS;
+    const unsigned ph = (unsigned)(kt / S) & 1u;
+    const bool xf = kt + A < KT;
+    T* nx = smem + ((kt + A) % S) * Cc::STAGE_ELEMS;
+    double2 x = make_double2(0.0, 0.0);
+    if (xf) {
+      mbar_wait(&full[(kt + A) % S], (unsigned)((kt + A) / S) & 1u);
+      x = *reinterpret_cast<const double2*>(nx + XS + xoff);
+    }
+    const T* st = smem + s * Cc::STAGE_ELEMS;
 #pragma unroll 1
-    for (int kk = 0; kk < C::BK; kk += C::VEC)
-      micro_step<C>(acc, st, st + C::BM * C::PITCH, ty, tx, kk);
+    for (int u = 0; u < Cc::TM; ++u) {
+      double2* pa = reinterpret_cast<double2*>(nx + roff + 16 * u * Cc::PITCH);
+      double2 a;
+      if (xf) a = *pa;
+      micro_step<Cc>(acc, st, st + Cc::BM * Cc::PITCH, ty, tx, u * Cc::VEC);
+      if (xf) {
+        a.x = Traits<double>::min(x.x, a.x);
+        a.y = Traits<double>::min(x.y, a.y);
+        *pa = a;
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
+    if (tid == 0 && kt + S < KT) {
+      mbar_wait(&empty[s], ph);
+      issue(kt + S);
+    }
   }
-  return true;
 }
 
 struct Maps {
   CUtensorMap a, p;  // rows / cols (same matrix, box 128 vectors) and pivot (box 1)
 };
 
+template <int S>
+using CS = Cfg<double, 8, 8, S, 1, 0>;
+
+// V: 0 tma2 S4, 1 prod S4, 2 own A1 S4, 3 own A0 S4, 4 own A1 S5, 5 own A1 S6,
+//    6 own A2 S6, 7 prod S6, 8 tma2 S6; gen (production loop with knobs), S6:
+//    9 D3, 10 D2 box but no transform, 11 D2 no fence, 12 D2 no box / transform
+//    (ready barriers only), 13 D4; ilv: 14 A1 S4, 15 A1 S5, 16 A1 S6, 17 A2 S6
+constexpr int kVars = 18;
+constexpr int kStagesOf[kVars] = {4, 4, 4, 4, 5, 6, 6, 6, 6, 6, 6, 6, 6, 6, 4, 5, 6, 6};
+
 template <int V>
-__global__ void __launch_bounds__(V == 3 ? kNTW : V == 4 ? kNTG : kNT, 1)
+__global__ void __launch_bounds__(kNT, 1)
     k_var(const __grid_constant__ Maps mp, int64_t n, int64_t n_f, double* out) {
+  using Cc = CS<kStagesOf[V]>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* smem = reinterpret_cast<double*>(smem_raw);
-  const int64_t tiles_n = (n + C::BN - 1) / C::BN;
+  const int64_t tiles_n = (n + Cc::BN - 1) / Cc::BN;
   const int64_t bi = blockIdx.x / tiles_n, bj = blockIdx.x % tiles_n;
-  const int64_t row0 = bi * C::BM, col0 = bj * C::BN;
+  const int64_t row0 = bi * Cc::BM, col0 = bj * Cc::BN;
   const int p = (int)pivot_of(bi, bj, n);
-  double acc[C::TM][C::TN];
-  if (V == 0) {
-    minplus_tile_tma<C>(&mp.a, (int)row0, &mp.a, (int)col0, n_f, acc, smem);
-  } else if (V == 1) {
-    minplus_tile_pivot_tma<C>(&mp.a, (int)row0, &mp.a, (int)col0, &mp.p, p, n_f, acc, smem);
-  } else if (V == 2) {
-    tile_warp_own(&mp.a, (int)row0, &mp.a, (int)col0, &mp.p, p, n_f, acc, smem);
-  } else if (V == 4) {
-    if (!tile_ws_wg(&mp.a, (int)row0, &mp.a, (int)col0, &mp.p, p, n_f, acc, smem)) return;
+  double acc[Cc::TM][Cc::TN];
+  if constexpr (V == 0 || V == 8) {
+    minplus_tile_tma<Cc>(&mp.a, (int)row0, &mp.a, (int)col0, n_f, acc, smem);
+  } else if constexpr (V == 1 || V == 7) {
+    minplus_tile_pivot_tma<Cc>(&mp.a, (int)row0, &mp.a, (int)col0, &mp.p, p, n_f, acc, smem);
+  } else if constexpr (V >= 14) {
+    tile_ilv<Cc, V == 17 ? 2 : 1>(&mp.a, (int)row0, &mp.a, (int)col0, &mp.p, p, n_f, acc, smem);
+  } else if constexpr (V >= 9) {
+    constexpr int D = V == 9 ? 3 : V == 13 ? 4 : 2;
+    constexpr int F = V == 10 ? 1 : V == 11 ? 2 : V == 12 ? 4 : 0;
+    tile_gen<Cc, D, F>(&mp.a, (int)row0, &mp.a, (int)col0, &mp.p, p, n_f, acc, smem);
   } else {
-    if (!tile_ws(&mp.a, (int)row0, &mp.a, (int)col0, &mp.p, p, n_f, acc, smem)) return;
+    constexpr int A = V == 3 ? 0 : V == 6 ? 2 : 1;
+    tile_own<Cc, A>(&mp.a, (int)row0, &mp.a, (int)col0, &mp.p, p, n_f, acc, smem);
   }
-  store_tile<C>(acc, out, n, row0, col0);
+  store_tile<Cc>(acc, out, n, row0, col0);
 }
 
 __global__ void k_fill(double* p, int64_t cnt) {
@@ -356,6 +347,7 @@ float timed(F&& launch, int reps) {
 int main(int argc, char** argv) {
   const int64_t n = argc > 1 ? atoll(argv[1]) : 8192;
   const int64_t n_f = argc > 2 ? atoll(argv[2]) : 10000;
+  const int mask = argc > 3 ? atoi(argv[3]) : (1 << kVars) - 1;
   const int64_t ld = (n_f + 31) / 32 * 32;
   double *W, *o1, *o2;
   cudaMalloc(&W, sizeof(double) * ld * n);
@@ -369,34 +361,56 @@ int main(int argc, char** argv) {
     printf("{\"error\": \"tensor map encode failed\"}\n");
     return 1;
   }
-  const int smem = C::SMEM_BYTES;
-  cudaFuncSetAttribute(k_var<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_var<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_var<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_var<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_var<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int64_t tiles = ((n + 127) / 128) * ((n + 127) / 128);
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const double useful = (double)n * n * n_f;
   std::vector<double> h1(n * n), h2(n * n);
-  const char* names[5] = {"tma2", "prod", "warp_own", "ws", "ws_wg"};
-  const void* fns[5] = {(const void*)k_var<0>, (const void*)k_var<1>, (const void*)k_var<2>,
-                        (const void*)k_var<3>, (const void*)k_var<4>};
+  const char* names[kVars] = {"tma2_s4", "prod_s4", "own_a1_s4", "own_a0_s4", "own_a1_s5",
+                              "own_a1_s6", "own_a2_s6", "prod_s6", "tma2_s6", "gen_d3_s6",
+                              "gen_box_noxf_s6", "gen_nofence_s6", "gen_nobox_s6",
+                              "gen_d4_s6", "ilv_a1_s4", "ilv_a1_s5", "ilv_a1_s6",
+                              "ilv_a2_s6"};
+  const void* fns[kVars] = {(const void*)k_var<0>, (const void*)k_var<1>, (const void*)k_var<2>,
+                            (const void*)k_var<3>, (const void*)k_var<4>, (const void*)k_var<5>,
+                            (const void*)k_var<6>, (const void*)k_var<7>, (const void*)k_var<8>,
+                            (const void*)k_var<9>, (const void*)k_var<10>, (const void*)k_var<11>,
+                            (const void*)k_var<12>, (const void*)k_var<13>, (const void*)k_var<14>,
+                            (const void*)k_var<15>, (const void*)k_var<16>, (const void*)k_var<17>};
+  for (int v = 0; v < kVars; ++v) {
+    const int sm = kStagesOf[v] * C::STAGE_ELEMS * (int)sizeof(double);
+    cudaFuncSetAttribute(fns[v], cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  }
   auto run = [&](int v, double* o) {
+    const int sm = kStagesOf[v] * C::STAGE_ELEMS * (int)sizeof(double);
     switch (v) {
-      case 0: k_var<0><<<(unsigned)tiles, kNT, smem>>>(mp, n, n_f, o); break;
-      case 1: k_var<1><<<(unsigned)tiles, kNT, smem>>>(mp, n, n_f, o); break;
-      case 2: k_var<2><<<(unsigned)tiles, kNT, smem>>>(mp, n, n_f, o); break;
-      case 3: k_var<3><<<(unsigned)tiles, kNTW, smem>>>(mp, n, n_f, o); break;
-      default: k_var<4><<<(unsigned)tiles, kNTG, smem>>>(mp, n, n_f, o); break;
+      case 0: k_var<0><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
+      case 1: k_var<1><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
+      case 2: k_var<2><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
+      case 3: k_var<3><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
+      case 4: k_var<4><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
+      case 5: k_var<5><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
+      case 6: k_var<6><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
+      case 7: k_var<7><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
+      case 8: k_var<8><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
+      case 9: k_var<9><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
+      case 10: k_var<10><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
+      case 11: k_var<11><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
+      case 12: k_var<12><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
+      case 13: k_var<13><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
+      case 14: k_var<14><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
+      case 15: k_var<15><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
+      case 16: k_var<16><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
+      default: k_var<17><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
     }
   };
-  run(1, o1);
+  if (mask & 2) run(1, o1);
+  else cudaMemset(o1, 0, 8 * n * n);
   cudaDeviceSynchronize();
   cudaMemcpy(h1.data(), o1, 8 * n * n, cudaMemcpyDeviceToHost);
   for (int round = 0; round < 2; ++round)
-    for (int v = 0; v < 5; ++v) {
+    for (int v = 0; v < kVars; ++v) {
+      if (!((mask >> v) & 1)) continue;
       cudaMemset(o2, 0xff, 8 * n * n);
       const float ms = timed([&] { run(v, o2); }, 3);
       cudaFuncAttributes fa;
