@@ -46,6 +46,80 @@ __device__ __forceinline__ T czek3_value(const Czek3Box& b, int64_t ai, int64_t 
   return zero ? T(0) : Traits<T>::div(Traits<T>::mul(T(1.5), n3), d);
 }
 
+// Eq. 1 epilogue of a single-pivot tile (every output has the same j = d.p0,
+// nr1 = nc1 = 0): the same values and checksum terms as czek3_value + the
+// generic loop in k_czek3, with the per-row terms (n_ij, s_i + s_j, the
+// triple index base of (i, j)) loaded once, and each column's eight n_ik
+// loads (ld.global.nc: no ordering against the value stores) issued together,
+// so the epilogue pays the table latency about once per column instead of
+// once per output
+// (measured: the generic loop cost 3.3% of a 10000-field tile,
+// tools/exp_box3.py, profiles/r02_3way_pivot/).
+template <class C>
+__device__ __forceinline__ void czek3_epilogue_single(const Czek3Box& b, const Tile3& d,
+                                                      const int64_t* __restrict__ out_pref,
+                                                      typename C::T (&acc)[C::TM][C::TN],
+                                                      Cks& c) {
+  using T = typename C::T;
+  constexpr int TM = C::TM, TN = C::TN;
+  const int ty = thread_ty(), tx = thread_tx();
+  const uint64_t nv = (uint64_t)b.n_v;
+  const int64_t j = d.p0, jb = j - b.b0;
+  const int64_t klo = max64(b.k0, j + 1), ncols = b.k1 - klo;
+  const int64_t ra = d.row0 - b.a0, kcb = d.col0 - b.c0;
+  const T* nab = static_cast<const T*>(b.NAB) + jb * b.ldAB + ra;
+  const T* sa = static_cast<const T*>(b.SA) + ra;
+  const T* nac = static_cast<const T*>(b.NAC) + ra + kcb * b.ldAC;
+  const T* nbc = static_cast<const T*>(b.NBC) + jb + kcb * b.ldBC;
+  const T* sc = static_cast<const T*>(b.SC) + kcb;
+  T* out = static_cast<T*>(b.vals);
+  const int64_t obase = out ? out_pref[j - b.j0] + (d.row0 - b.i0) * ncols + (d.col0 - klo) : 0;
+  const T sj = __ldg(static_cast<const T*>(b.SB) + jb);
+  T nij[TM], sij[TM];
+  uint64_t bij[TM];  // triple_index(i, j, j + 1): add k - j - 1 for (i, j, k)
+#pragma unroll
+  for (int mi = 0; mi < TM; ++mi) {
+    const int li = ty + 16 * mi;
+    const bool ok = li < d.nr0;
+    nij[mi] = ok ? __ldg(nab + li) : T(0);
+    sij[mi] = ok ? Traits<T>::add(__ldg(sa + li), sj) : T(0);
+    const uint64_t i = (uint64_t)(d.row0 + li);
+    bij[mi] = choose3(nv) - choose3(nv - i) +
+              pair_index((uint64_t)j - i - 1, (uint64_t)j - i, nv - i - 1);
+  }
+  auto load_col = [&](int nk, T (&nik)[TM], T& njk, T& sk) {
+    const int lk = tx + 16 * nk;
+    const bool okc = lk < d.nc0;
+    njk = okc ? __ldg(nbc + lk * b.ldBC) : T(0);
+    sk = okc ? __ldg(sc + lk) : T(0);
+#pragma unroll
+    for (int mi = 0; mi < TM; ++mi)
+      nik[mi] = (okc && ty + 16 * mi < d.nr0) ? __ldg(nac + (ty + 16 * mi) + lk * b.ldAC) : T(0);
+  };
+#pragma unroll
+  for (int nk = 0; nk < TN; ++nk) {
+    const int lk = tx + 16 * nk;
+    if (lk >= d.nc0) continue;
+    T nik[TM], njk, sk;
+    load_col(nk, nik, njk, sk);
+    const uint64_t kj = (uint64_t)(d.col0 + lk - j - 1);
+#pragma unroll
+    for (int mi = 0; mi < TM; ++mi) {
+      const int li = ty + 16 * mi;
+      if (li >= d.nr0) continue;
+      // metrics3.py:38-44, canonical roles: 1.5 (((n_ij + n_ik) + n_jk) - n_ijk) / ((s_i + s_j) + s_k)
+      const T n3 = Traits<T>::sub(Traits<T>::add(Traits<T>::add(nij[mi], nik[mi]), njk),
+                                  acc[mi][nk]);
+      const T dd = Traits<T>::add(sij[mi], sk);
+      const bool zero = dd == T(0);
+      const T v = zero ? T(0) : Traits<T>::div(Traits<T>::mul(T(1.5), n3), dd);
+      if (out) out[obase + li * ncols + lk] = v;
+      c.term(bij[mi] + kj, Traits<T>::bits(v));
+      c.deg += zero ? 1ull : 0ull;
+    }
+  }
+}
+
 // The 3-way mainloop of one (possibly packed) tile: the 2-way pipeline with
 // the pivot min applied to each landed stage. Each thread stages the same
 // A rows (tid/8 + 32r) and B columns every stage, so their sources are
@@ -192,6 +266,12 @@ __global__ void __launch_bounds__(kNT, C::MINB)
   // decoded again (measured: keeping the tile state live across the mainloop
   // costs registers and ~4% of the mainloop's issue rate)
   const Tile3 d = box3_decode<C::BM, C::BN, PACKED>(b, tile_pref, nJ, blockIdx.x);
+  if constexpr (!RAW && !PACKED) {
+    Cks c;
+    czek3_epilogue_single<C>(b, d, out_pref, acc, c);
+    cks_block_flush<kNT>(b.acc, c);
+    return;
+  }
 
   T* out = static_cast<T*>(b.vals);
   const uint64_t nv = (uint64_t)b.n_v;

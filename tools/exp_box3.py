@@ -2,7 +2,8 @@
 
     python tools/exp_box3.py [n_f]
 
-Times psim_czek3_box on boxes of one resident 6144-vector block and prints,
+Times psim_czek3_box (and psim_czek3_box_numerators: the same tiles with
+the raw n_ijk stored instead of the Eq. 1 epilogue) on boxes of one resident 6144-vector block and prints,
 per box, useful and padded-tile cmp/clk/SM (clock 1965 MHz assumed; the bench
 samples clocks), so the kernel's own overhead can be separated from tile
 padding: a volume box (i < j < k ranges disjoint: every tile full) vs
@@ -57,18 +58,20 @@ def main():
         vals = torch.empty(n_out, dtype=torch.float64, device=dev)
         b = box_struct(box, blocks, sums, tables, n_f, n, vals, acc)
         N.call("psim_czek3_box", N.F64, C.byref(b), D.stream_ptr())
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        N.call("psim_czek3_box", N.F64, C.byref(b), D.stream_ptr())
-        e1.record()
-        torch.cuda.synchronize()
-        s = e0.elapsed_time(e1) * 1e-3
-        clk = sms * 1.965e9 * s
-        print(json.dumps({"box": name, "ms": s * 1e3, "tiles": n_tiles,
-                          "fill": n_out / (n_tiles * 16384),
-                          "useful_cmp_clk_sm": n_out * n_f / clk,
-                          "padded_cmp_clk_sm": n_tiles * 16384 * n_f / clk}), flush=True)
-
+        for fn in ("psim_czek3_box", "psim_czek3_box_numerators"):
+            if fn != "psim_czek3_box":  # raw n_ijk (no epilogue) into the same buffer
+                N.call(fn, N.F64, C.byref(b), D.stream_ptr())
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            N.call(fn, N.F64, C.byref(b), D.stream_ptr())
+            e1.record()
+            torch.cuda.synchronize()
+            s = e0.elapsed_time(e1) * 1e-3
+            clk = sms * 1.965e9 * s
+            print(json.dumps({"box": name, "fn": fn, "ms": s * 1e3, "tiles": n_tiles,
+                              "fill": n_out / (n_tiles * 16384),
+                              "useful_cmp_clk_sm": n_out * n_f / clk,
+                              "padded_cmp_clk_sm": n_tiles * 16384 * n_f / clk}), flush=True)
 
 if __name__ == "__main__":
     main()
