@@ -281,6 +281,115 @@ __device__ __forceinline__ void tile_ilv(const void* mapA, int a_row0, const voi
   }
 }
 
+// ---- w16: thread grid with 2 rows x 16 columns per warp (ty = 2w + lane/16,
+// tx = lane%16): every A row is read by exactly one warp, so the per-warp
+// rewrite has no duplicate (4 chunks per lane per stage instead of 8)
+__device__ __forceinline__ int w16_ty() { return (threadIdx.x >> 5) * 2 + ((threadIdx.x & 31) >> 4); }
+__device__ __forceinline__ int w16_tx() { return threadIdx.x & 15; }
+
+template <class Cc, bool PIV>
+__device__ __forceinline__ void tile_w16(const void* mapA, int a_row0, const void* mapC,
+                                         int c_row0, const void* mapB, int p_row, int64_t n_f,
+                                         double (&acc)[Cc::TM][Cc::TN], double* smem) {
+  constexpr int S = Cc::STAGES;
+  constexpr int XS = (Cc::BM + Cc::BN) * Cc::PITCH;
+  constexpr unsigned kBytes = (Cc::BM + Cc::BN + (PIV ? 1 : 0)) * Cc::PITCH * sizeof(T);
+  constexpr int A = 1;
+  __shared__ __align__(8) uint64_t full[S], empty[S];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kNT / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+#pragma unroll
+  for (int m = 0; m < Cc::TM; ++m)
+#pragma unroll
+    for (int n = 0; n < Cc::TN; ++n) acc[m][n] = 0.0;
+  __syncthreads();
+  const int KT = (int)((n_f + Cc::BK - 1) / Cc::BK);
+  auto issue = [&](int kt) {
+    const int s = kt % S;
+    T* st = smem + s * Cc::STAGE_ELEMS;
+    mbar_expect_tx(&full[s], kBytes);
+    tma_box(st, mapA, kt * Cc::BK, a_row0, &full[s]);
+    tma_box(st + Cc::BM * Cc::PITCH, mapC, kt * Cc::BK, c_row0, &full[s]);
+    if (PIV) tma_box(st + XS, mapB, kt * Cc::BK, p_row, &full[s]);
+  };
+  // chunk h (0..3) of this lane: row 2w + (idx & 1) + 16 (idx >> 1), idx = lane/8 + 4h
+  const int xoff = (lane & 7) * Cc::VEC;
+  auto roff = [&](int h) {
+    const int idx = (lane >> 3) + 4 * h;
+    return (2 * w + (idx & 1) + 16 * (idx >> 1)) * Cc::PITCH + xoff;
+  };
+  if (tid == 0)
+    for (int kt = 0; kt < S && kt < KT; ++kt) issue(kt);
+  if (PIV && KT > 0) {
+    mbar_wait(&full[0], 0u);
+    T* st = smem;
+    const double2 x = *reinterpret_cast<const double2*>(st + XS + xoff);
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      double2* p = reinterpret_cast<double2*>(st + roff(h));
+      double2 a = *p;
+      a.x = Traits<double>::min(x.x, a.x);
+      a.y = Traits<double>::min(x.y, a.y);
+      *p = a;
+    }
+    __syncwarp();
+  }
+  const int ty = w16_ty(), tx = w16_tx();
+  for (int kt = 0; kt < KT; ++kt) {
+    const int s = kt % S;
+    const unsigned ph = (unsigned)(kt / S) & 1u;
+    const bool xf = PIV && kt + A < KT;
+    T* nx = smem + ((kt + A) % S) * Cc::STAGE_ELEMS;
+    double2 x = make_double2(0.0, 0.0);
+    if (xf) {
+      mbar_wait(&full[(kt + A) % S], (unsigned)((kt + A) / S) & 1u);
+      x = *reinterpret_cast<const double2*>(nx + XS + xoff);
+    } else if (!PIV) {
+      mbar_wait(&full[s], ph);
+    }
+    const T* st = smem + s * Cc::STAGE_ELEMS;
+#pragma unroll 1
+    for (int u = 0; u < Cc::TM; ++u) {
+      double2* pa = reinterpret_cast<double2*>(nx + roff(u >> 1));
+      double2 a;
+      const bool doit = xf && !(u & 1);
+      if (doit) a = *pa;
+      micro_step<Cc>(acc, st, st + Cc::BM * Cc::PITCH, ty, tx, u * Cc::VEC);
+      if (doit) {
+        a.x = Traits<double>::min(x.x, a.x);
+        a.y = Traits<double>::min(x.y, a.y);
+        *pa = a;
+      }
+    }
+    if (PIV) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (tid == 0 && kt + S < KT) {
+      mbar_wait(&empty[s], ph);
+      issue(kt + S);
+    }
+  }
+}
+
+template <class Cc>
+__device__ __forceinline__ void store_tile_w16(double (&acc)[Cc::TM][Cc::TN], double* out,
+                                               int64_t n, int64_t row0, int64_t col0) {
+  const int ty = w16_ty(), tx = w16_tx();
+#pragma unroll
+  for (int m = 0; m < Cc::TM; ++m)
+#pragma unroll
+    for (int q = 0; q < Cc::TN; ++q) {
+      const int64_t i = row0 + ty + 16 * m, j = col0 + tx + 16 * q;
+      if (i < n && j < n) out[i + j * n] = acc[m][q];
+    }
+}
+
 struct Maps {
   CUtensorMap a, p;  // rows / cols (same matrix, box 128 vectors) and pivot (box 1)
 };
@@ -291,9 +400,10 @@ using CS = Cfg<double, 8, 8, S, 1, 0>;
 // V: 0 tma2 S4, 1 prod S4, 2 own A1 S4, 3 own A0 S4, 4 own A1 S5, 5 own A1 S6,
 //    6 own A2 S6, 7 prod S6, 8 tma2 S6; gen (production loop with knobs), S6:
 //    9 D3, 10 D2 box but no transform, 11 D2 no fence, 12 D2 no box / transform
-//    (ready barriers only), 13 D4; ilv: 14 A1 S4, 15 A1 S5, 16 A1 S6, 17 A2 S6
-constexpr int kVars = 18;
-constexpr int kStagesOf[kVars] = {4, 4, 4, 4, 5, 6, 6, 6, 6, 6, 6, 6, 6, 6, 4, 5, 6, 6};
+//    (ready barriers only), 13 D4; ilv: 14 A1 S4, 15 A1 S5, 16 A1 S6, 17 A2 S6;
+//    w16 mapping, S4: 18 2-way (no pivot), 19 ilv A1
+constexpr int kVars = 20;
+constexpr int kStagesOf[kVars] = {4, 4, 4, 4, 5, 6, 6, 6, 6, 6, 6, 6, 6, 6, 4, 5, 6, 6, 4, 4};
 
 template <int V>
 __global__ void __launch_bounds__(kNT, 1)
@@ -306,13 +416,17 @@ __global__ void __launch_bounds__(kNT, 1)
   const int64_t row0 = bi * Cc::BM, col0 = bj * Cc::BN;
   const int p = (int)pivot_of(bi, bj, n);
   double acc[Cc::TM][Cc::TN];
-  if constexpr (V == 0 || V == 8) {
+  if constexpr (V == 18 || V == 19) {
+    tile_w16<Cc, V == 19>(&mp.a, (int)row0, &mp.a, (int)col0, &mp.p, p, n_f, acc, smem);
+    store_tile_w16<Cc>(acc, out, n, row0, col0);
+    return;
+  } else if constexpr (V == 0 || V == 8) {
     minplus_tile_tma<Cc>(&mp.a, (int)row0, &mp.a, (int)col0, n_f, acc, smem);
   } else if constexpr (V == 1 || V == 7) {
     minplus_tile_pivot_tma<Cc>(&mp.a, (int)row0, &mp.a, (int)col0, &mp.p, p, n_f, acc, smem);
-  } else if constexpr (V >= 14) {
+  } else if constexpr (V >= 14 && V < 18) {
     tile_ilv<Cc, V == 17 ? 2 : 1>(&mp.a, (int)row0, &mp.a, (int)col0, &mp.p, p, n_f, acc, smem);
-  } else if constexpr (V >= 9) {
+  } else if constexpr (V >= 9 && V < 14) {
     constexpr int D = V == 9 ? 3 : V == 13 ? 4 : 2;
     constexpr int F = V == 10 ? 1 : V == 11 ? 2 : V == 12 ? 4 : 0;
     tile_gen<Cc, D, F>(&mp.a, (int)row0, &mp.a, (int)col0, &mp.p, p, n_f, acc, smem);
@@ -370,13 +484,14 @@ int main(int argc, char** argv) {
                               "own_a1_s6", "own_a2_s6", "prod_s6", "tma2_s6", "gen_d3_s6",
                               "gen_box_noxf_s6", "gen_nofence_s6", "gen_nobox_s6",
                               "gen_d4_s6", "ilv_a1_s4", "ilv_a1_s5", "ilv_a1_s6",
-                              "ilv_a2_s6"};
+                              "ilv_a2_s6", "w16_tma2_s4", "w16_ilv_a1_s4"};
   const void* fns[kVars] = {(const void*)k_var<0>, (const void*)k_var<1>, (const void*)k_var<2>,
                             (const void*)k_var<3>, (const void*)k_var<4>, (const void*)k_var<5>,
                             (const void*)k_var<6>, (const void*)k_var<7>, (const void*)k_var<8>,
                             (const void*)k_var<9>, (const void*)k_var<10>, (const void*)k_var<11>,
                             (const void*)k_var<12>, (const void*)k_var<13>, (const void*)k_var<14>,
-                            (const void*)k_var<15>, (const void*)k_var<16>, (const void*)k_var<17>};
+                            (const void*)k_var<15>, (const void*)k_var<16>, (const void*)k_var<17>,
+                            (const void*)k_var<18>, (const void*)k_var<19>};
   for (int v = 0; v < kVars; ++v) {
     const int sm = kStagesOf[v] * C::STAGE_ELEMS * (int)sizeof(double);
     cudaFuncSetAttribute(fns[v], cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
@@ -401,7 +516,9 @@ int main(int argc, char** argv) {
       case 14: k_var<14><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
       case 15: k_var<15><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
       case 16: k_var<16><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
-      default: k_var<17><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
+      case 17: k_var<17><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
+      case 18: k_var<18><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
+      default: k_var<19><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
     }
   };
   if (mask & 2) run(1, o1);
