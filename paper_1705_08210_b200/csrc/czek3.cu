@@ -37,10 +37,12 @@ __device__ __forceinline__ T czek3_value(const Czek3Box& b, int64_t ai, int64_t 
   const T* SA = static_cast<const T*>(b.SA);
   const T* SB = static_cast<const T*>(b.SB);
   const T* SC = static_cast<const T*>(b.SC);
-  const T nij = static_cast<const T*>(b.NAB)[ai + jb * b.ldAB];
-  const T nik = static_cast<const T*>(b.NAC)[ai + kc * b.ldAC];
-  const T njk = static_cast<const T*>(b.NBC)[jb + kc * b.ldBC];
-  const T d = Traits<T>::add(Traits<T>::add(SA[ai], SB[jb]), SC[kc]);
+  // ld.global.nc: the tables are read-only here, so the loads of consecutive
+  // outputs need not wait behind the value stores
+  const T nij = __ldg(static_cast<const T*>(b.NAB) + ai + jb * b.ldAB);
+  const T nik = __ldg(static_cast<const T*>(b.NAC) + ai + kc * b.ldAC);
+  const T njk = __ldg(static_cast<const T*>(b.NBC) + jb + kc * b.ldBC);
+  const T d = Traits<T>::add(Traits<T>::add(__ldg(SA + ai), __ldg(SB + jb)), __ldg(SC + kc));
   const T n3 = Traits<T>::sub(Traits<T>::add(Traits<T>::add(nij, nik), njk), n_ijk);
   zero = (d == T(0));
   return zero ? T(0) : Traits<T>::div(Traits<T>::mul(T(1.5), n3), d);
