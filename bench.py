@@ -466,6 +466,28 @@ class RuntimeBench:
     def pieces(self):
         return self.run.outcome().pieces
 
+    def scratch_box(self):
+        """3-way: (BoxPiece, device tensor) of the box whose values the
+        runtime's scratch buffer still holds after the last step
+        (psim_out_t.scratch_piece / scratch_vals), or None."""
+        import torch
+
+        from paper_1705_08210_b200.plan import Box, box_count
+
+        out = self.run.out
+        if out is None or out.scratch_piece < 0 or not out.scratch_vals:
+            return None
+        pc = self.run.outcome().pieces[out.scratch_piece]
+        n = box_count(Box((0, 0, 0), pc.i0, pc.i1, pc.j0, pc.j1, pc.k0, pc.k1))
+        typestr = "<f8" if self.prob.precision == "double" else "<f4"
+
+        class _View:  # the scratch values as a CUDA array (no copy)
+            __cuda_array_interface__ = {"shape": (n,), "typestr": typestr,
+                                        "data": (out.scratch_vals, True), "version": 3}
+
+        return pc, torch.as_tensor(_View(), device=torch.device("cuda",
+                                                                torch.cuda.current_device()))
+
     def checksum_hex(self) -> str:
         out = self.run.out
         return format((out.checksum[1] << 64) | out.checksum[0], "032x")
@@ -534,10 +556,16 @@ def sampled_parity(runner, prob, bits, world, dev) -> dict:
         how = (f"per value piece: sampled rows x sampled columns ({side} each), values "
                f"recomputed from their columns by oracle.propsim_np.pair_values_grid "
                f"(n_pf={n_pf} ordered fold)")
-    elif hasattr(runner, "stage_boxes"):  # Resident3: the last pivot chunk is in runner.buf
+    elif hasattr(runner, "stage_boxes") or (hasattr(runner, "scratch_box")
+                                            and runner.scratch_box() is not None):
+        # Resident3: the last pivot chunk is in runner.buf; the multi-GPU
+        # runtime: the last box of this rank is in its scratch buffer
         from paper_1705_08210_b200.plan import box_count
 
-        box = runner.stage_boxes[-1][-1]
+        if hasattr(runner, "stage_boxes"):
+            box, buf = runner.stage_boxes[-1][-1], runner.buf
+        else:
+            box, buf = runner.scratch_box()
         off, offs = 0, {}
         for j in range(box.j0, box.j1):
             offs[j] = off
@@ -559,14 +587,14 @@ def sampled_parity(runner, prob, bits, world, dev) -> dict:
             want = O.triple_values_grid(VI, xj, VK).ravel()
             ii, kk = np.meshgrid(rows, cols, indexing="ij")
             pos = offs[j] + (ii - box.i0) * (box.k1 - klo) + (kk - klo)
-            got = D.to_host(runner.buf[torch.as_tensor(pos.ravel(), device=runner.buf.device)])
+            got = D.to_host(buf[torch.as_tensor(pos.ravel(), device=buf.device)])
             mismatches += int((got.view(np.uint8).reshape(len(got), -1)
                                != want.view(np.uint8).reshape(len(want), -1)).any(axis=1).sum())
             sampled += len(got)
         how = (f"{len(js)} pivots of the last pivot chunk x (sampled rows x sampled columns), "
                "recomputed from their columns by oracle.propsim_np.triple_values_grid")
-    else:
-        return {"sampled": 0, "mismatches": 0, "note": "values not retained by this harness"}
+    else:  # (still joins the sum over ranks below: other ranks may hold values)
+        how = "values not retained by this harness on rank 0"
     if world > 1:
         import torch.distributed as dist
 

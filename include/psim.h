@@ -319,6 +319,11 @@ typedef struct psim_out {
   psim_traffic_t traffic;    /* this rank */
   double kernel_seconds;     /* this rank: CUDA-event time of its fused min-plus launches */
   int64_t kernel_grids;      /* ... and how many launch groups (task groups / boxes) */
+  /* PSIM_RUN_VALUES_SCRATCH runs of psim_run3: the piece whose values the
+   * workspace scratch holds when the call returns (-1: none) and their
+   * device address (pivot-major, as out->vals would hold that piece). */
+  int64_t scratch_piece;
+  const void* scratch_vals;
 } psim_out_t;
 
 typedef struct psim_plan {

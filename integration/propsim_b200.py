@@ -57,7 +57,8 @@ class _Out(C.Structure):
                 ("rank_traffic", C.POINTER(_Traffic)), ("n_pieces", _i64), ("n_vals", _i64),
                 ("checksum", C.c_uint64 * 2), ("count", _i64), ("degenerate", _i64),
                 ("local_count", _i64), ("elapsed", C.c_double), ("traffic", _Traffic),
-                ("kernel_seconds", C.c_double), ("kernel_grids", _i64)]
+                ("kernel_seconds", C.c_double), ("kernel_grids", _i64),
+                ("scratch_piece", _i64), ("scratch_vals", _vp)]
 
 
 class _Plan(C.Structure):

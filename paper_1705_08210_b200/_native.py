@@ -100,6 +100,7 @@ class Out(C.Structure):
         ("count", c_i64), ("degenerate", c_i64), ("local_count", c_i64),
         ("elapsed", C.c_double), ("traffic", Traffic),
         ("kernel_seconds", C.c_double), ("kernel_grids", c_i64),
+        ("scratch_piece", c_i64), ("scratch_vals", c_vp),
     ]
 
 

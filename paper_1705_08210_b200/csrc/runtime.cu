@@ -321,6 +321,10 @@ struct Rank {
   std::vector<psim_piece_t> pieces;
   int64_t n_vals = 0, local_count = 0;
   std::vector<cudaEvent_t> kev;  // (start, end) pairs around the fused min-plus launches
+  // PSIM_RUN_VALUES_SCRATCH: the piece whose values the scratch buffer holds
+  // at the end of the run, and where (reported in psim_out_t)
+  int64_t scratch_piece = -1;
+  const void* scratch_vals = nullptr;
 
   bool kmark() {  // one event on the compute stream
     cudaEvent_t e;
@@ -572,6 +576,8 @@ struct Rank {
         out->kernel_seconds += kms * 1e-3;
     }
     out->local_count = local_count;
+    out->scratch_piece = scratch_piece;
+    out->scratch_vals = scratch_vals;
     out->n_vals = n_vals;
     out->n_pieces = (int64_t)pieces.size();
     if (out->pieces) std::copy(pieces.begin(), pieces.end(), out->pieces);
@@ -1098,6 +1104,10 @@ struct Run3 : Rank {
       if (g->n_pf == 1) {
         psim_box3_t s = box_struct(b, vals, true);
         if (!kmark() || !S.psim(psim_czek3_box(dtype, &s, st)) || !kmark()) return false;
+        if (scratch) {
+          scratch_piece = piece_of[bi];
+          scratch_vals = scratch;
+        }
         continue;
       }
       // field split (metrics3.py:163-164): raw n_ijk of this slab, the ordered
