@@ -483,7 +483,7 @@ class RuntimeBench:
 
         class _View:  # the scratch values as a CUDA array (no copy)
             __cuda_array_interface__ = {"shape": (n,), "typestr": typestr,
-                                        "data": (out.scratch_vals, True), "version": 3}
+                                        "data": (out.scratch_vals, False), "version": 3}
 
         return pc, torch.as_tensor(_View(), device=torch.device("cuda",
                                                                 torch.cuda.current_device()))
