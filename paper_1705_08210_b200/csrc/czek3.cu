@@ -234,7 +234,7 @@ __device__ __forceinline__ void minplus_tile3(const Czek3Box& b, const Tile3& d,
 // PACKED selects the grid of two-pivot tiles (its own launch, so each grid
 // runs a single mainloop body).
 // Tensor maps of a box's three blocks for TMA staging of single-pivot tiles
-// (minplus_tile_pivot_tma): I rows of A, K columns of C (PITCH x BM / BN
+// (minplus_tile_pivot_ilv): I rows of A, K columns of C (PITCH x BM / BN
 // boxes), and the pivot vector of B (PITCH x 1).
 struct Box3Tma {
   int on;

@@ -1,5 +1,5 @@
 // Host side of TMA staging (minplus.cuh: minplus_tile_tma /
-// minplus_tile_pivot_tma): tensor maps of the vector blocks. The encoder
+// minplus_tile_pivot_ilv): tensor maps of the vector blocks. The encoder
 // comes from the driver through the runtime (no libcuda link);
 // PSIM_NO_TMA=1 keeps the cp.async loaders (read per launch, for A/B runs).
 #pragma once

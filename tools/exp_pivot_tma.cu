@@ -35,6 +35,90 @@ using namespace psim;
 using C = Prod<double>::C;
 using T = double;
 
+// The round-2 first production loop ("prod", moved here from csrc/minplus.cuh
+// when minplus_tile_pivot_ilv replaced it): as minplus_tile_tma plus the
+// pivot chunk (a third box: PITCH fields of the pivot vector, zero past n_f)
+// and the pivot min A[r][q] <- min(x_j[q], A[r][q]) applied in shared memory
+// (xj_columns, mingemm.py:225-234) by every thread to its share of the stage,
+// D stages ahead of the compute: warps publish the transformed stage on a
+// per-stage "ready" mbarrier, so the transform needs no CTA-wide barrier.
+template <class C>
+__device__ __forceinline__ void minplus_tile_pivot_tma(const void* mapA, int a_row0,
+                                                       const void* mapC, int c_row0,
+                                                       const void* mapB, int p_row,
+                                                       int64_t n_f,
+                                                       typename C::T (&acc)[C::TM][C::TN],
+                                                       typename C::T* smem) {
+  using T = typename C::T;
+  constexpr int S = C::STAGES;
+  constexpr int XS = (C::BM + C::BN) * C::PITCH;  // pivot slot inside a stage
+  constexpr unsigned kBytes = (C::BM + C::BN + 1) * C::PITCH * sizeof(T);
+  __shared__ __align__(8) uint64_t full[S], ready[S], empty[S];
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&ready[s], kNT / 32);
+      mbar_init(&empty[s], kNT / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+#pragma unroll
+  for (int m = 0; m < C::TM; ++m)
+#pragma unroll
+    for (int n = 0; n < C::TN; ++n) acc[m][n] = T(0);
+  __syncthreads();
+  const int KT = (int)((n_f + C::BK - 1) / C::BK);
+  auto issue = [&](int kt) {
+    const int s = kt % S;
+    T* st = smem + s * C::STAGE_ELEMS;
+    mbar_expect_tx(&full[s], kBytes);
+    tma_box(st, mapA, kt * C::BK, a_row0, &full[s]);
+    tma_box(st + C::BM * C::PITCH, mapC, kt * C::BK, c_row0, &full[s]);
+    tma_box(st + XS, mapB, kt * C::BK, p_row, &full[s]);
+  };
+  // land stage kt, apply the pivot min to this thread's chunks, publish it
+  auto transform = [&](int kt) {
+    const int s = kt % S;
+    mbar_wait(&full[s], (unsigned)(kt / S) & 1u);
+    T* st = smem + s * C::STAGE_ELEMS;
+    stage_pivot_min<C>(st, st + XS);
+    // generic-proxy writes before the slot is refilled by the async proxy
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ready[s]);
+  };
+  // transform D stages ahead of the compute: a warp may then run up to D
+  // stages ahead of the slowest one before it waits on a "ready" barrier (the
+  // stage D ahead was issued S - D iterations earlier, so it has landed)
+  constexpr int D = S >= 4 ? 2 : 1;
+  if (tid == 0)
+    for (int kt = 0; kt < S && kt < KT; ++kt) issue(kt);
+  for (int kt = 0; kt < D && kt < KT; ++kt) transform(kt);
+  const int ty = thread_ty(), tx = thread_tx();
+  for (int kt = 0; kt < KT; ++kt) {
+    const int s = kt % S;
+    const unsigned ph = (unsigned)(kt / S) & 1u;
+    if (kt + D < KT) transform(kt + D);
+    mbar_wait(&ready[s], ph);
+    const T* st = smem + s * C::STAGE_ELEMS;
+#ifdef PSIM_PIVOT_TMA_KKU
+    constexpr int U = PSIM_PIVOT_TMA_KKU;
+#else
+    constexpr int U = C::KKU;
+#endif
+#pragma unroll U
+    for (int kk = 0; kk < C::BK; kk += C::VEC)
+      micro_step<C>(acc, st, st + C::BM * C::PITCH, ty, tx, kk);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (tid == 0 && kt + S < KT) {
+      mbar_wait(&empty[s], ph);
+      issue(kt + S);
+    }
+  }
+}
+
 __device__ __forceinline__ int64_t pivot_of(int64_t bi, int64_t bj, int64_t n) {
   return (bi * 131 + bj * 17) % n;
 }
