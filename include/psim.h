@@ -102,6 +102,12 @@ typedef struct psim_box3 {
 /* --- library / device ----------------------------------------------------- */
 int psim_version(void);
 const char* psim_last_error(void);
+/* Layout of the public structs, for bindings that restate them (ctypes,
+ * cgo, ...): out[2k] = sizeof, out[2k + 1] = offsetof its last member, for
+ * k = psim_block2_t, psim_box3_t, psim_problem_t, psim_grid_t, psim_piece_t,
+ * psim_traffic_t, psim_out_t, psim_plan_t, psim_msg_t (in that order).
+ * Writes min(n, 9) pairs; returns 9. */
+int psim_abi_layout(int64_t* out, int n);
 /* SM count and compute capability of the current device. */
 int psim_device_info(int* sm_count, int* cc_major, int* cc_minor);
 /* CTA output tile (rows x cols) of the min-plus kernels for a dtype. */

@@ -124,10 +124,19 @@ INPUT_RANDOM_EXACT, INPUT_ANALYTIC, INPUT_UNIFORM, INPUT_DEVICE, INPUT_HOST = ra
 RUN_BALANCE_REFERENCE, RUN_VALUES_SCRATCH, RUN_NO_STREAM = 1, 2, 4
 
 
+# ctypes mirrors of the public structs in psim_abi_layout order (checked
+# against the library's sizeof / offsetof by tests/test_capi.py)
+def abi_mirrors():
+    return [(Block2, "acc"), (Box3, "acc"), (Problem, "ld"), (Grid, "n_st"), (Piece, "v"),
+            (Traffic, "nbytes"), (Out, "scratch_vals"), (Plan, "workspace_bytes"),
+            (Msg, "slot")]
+
+
 # name -> (restype, argtypes); every symbol declared in include/psim.h
 SIGNATURES = {
     "psim_version": (C.c_int, []),
     "psim_last_error": (C.c_char_p, []),
+    "psim_abi_layout": (C.c_int, [C.POINTER(c_i64), C.c_int]),
     "psim_device_info": (C.c_int, [C.POINTER(C.c_int)] * 3),
     "psim_tile_shape": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "psim_gen_random_exact": (

@@ -1,7 +1,9 @@
 // extern "C" boundary of libpsim (declared in include/psim.h): argument
 // validation, error-status mapping and the host-side planning of 3-way
 // boxes. No kernel code lives here.
+#include <algorithm>
 #include <atomic>
+#include <cstddef>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -99,6 +101,23 @@ int set_error(int code, const char* fmt, ...) {
 extern "C" {
 
 int psim_version(void) { return PSIM_VERSION; }
+
+int psim_abi_layout(int64_t* out, int n) {
+  const int64_t t[] = {
+      (int64_t)sizeof(psim_block2_t),  (int64_t)offsetof(psim_block2_t, acc),
+      (int64_t)sizeof(psim_box3_t),    (int64_t)offsetof(psim_box3_t, acc),
+      (int64_t)sizeof(psim_problem_t), (int64_t)offsetof(psim_problem_t, ld),
+      (int64_t)sizeof(psim_grid_t),    (int64_t)offsetof(psim_grid_t, n_st),
+      (int64_t)sizeof(psim_piece_t),   (int64_t)offsetof(psim_piece_t, v),
+      (int64_t)sizeof(psim_traffic_t), (int64_t)offsetof(psim_traffic_t, nbytes),
+      (int64_t)sizeof(psim_out_t),     (int64_t)offsetof(psim_out_t, scratch_vals),
+      (int64_t)sizeof(psim_plan_t),    (int64_t)offsetof(psim_plan_t, workspace_bytes),
+      (int64_t)sizeof(psim_msg_t),     (int64_t)offsetof(psim_msg_t, slot),
+  };
+  constexpr int kStructs = (int)(sizeof(t) / sizeof(t[0]) / 2);
+  for (int k = 0; out && k < 2 * std::min(n, kStructs); ++k) out[k] = t[k];
+  return kStructs;
+}
 
 const char* psim_last_error(void) { return g_err; }
 

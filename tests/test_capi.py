@@ -136,3 +136,38 @@ def test_box3_tiles_cover_every_triple_once(lib, code):
                 seen[I - box.i0, jj - box.j0, K - box.k0] += 1  # cells of a tile are distinct
         assert seen.max() == 1, box
         assert int(seen.sum()) == box_count(box), box
+
+
+def _layout(lib):
+    from paper_1705_08210_b200 import _native
+
+    buf = (C.c_int64 * 18)()
+    assert "psim_abi_layout" in _native.SIGNATURES
+    n = lib.psim_abi_layout(buf, 9)
+    assert n == 9
+    return [(buf[2 * k], buf[2 * k + 1]) for k in range(9)]
+
+
+def test_ctypes_mirrors_match_the_c_structs(lib):
+    """Every ctypes restatement of a public struct (the package's _native and
+    the torch-free reference-side binding) has the C sizeof and the C offset
+    of its last member: a field added on one side only fails here, not as
+    silent memory corruption on the GPU box."""
+    from paper_1705_08210_b200 import _native
+
+    want = _layout(lib)
+    for (cls, last), (size, off) in zip(_native.abi_mirrors(), want):
+        assert C.sizeof(cls) == size, (cls.__name__, C.sizeof(cls), size)
+        assert getattr(cls, last).offset == off, (cls.__name__, last)
+    import sys
+
+    sys.path.insert(0, str(ROOT / "integration"))
+    import propsim_b200 as B
+
+    order = {"_Problem": 2, "_Grid": 3, "_Piece": 4, "_Traffic": 5, "_Out": 6, "_Plan": 7}
+    last = {"_Problem": "ld", "_Grid": "n_st", "_Piece": "v", "_Traffic": "nbytes",
+            "_Out": "scratch_vals", "_Plan": "workspace_bytes"}
+    for name, k in order.items():
+        cls = getattr(B, name)
+        assert C.sizeof(cls) == want[k][0], name
+        assert getattr(cls, last[name]).offset == want[k][1], name
