@@ -75,9 +75,23 @@ template <>
 struct Prod<double> {
   using C = Cfg<double, 8, 8, 4, 1, 0>;  // 128 x 128, 1 CTA/SM (254 regs)
 };
+// (-DPSIM_F32_TN= / _STAGES= / _MINB= / _VAR= override it for A/B builds,
+// tools/build_variant.sh)
+#ifndef PSIM_F32_TN
+#define PSIM_F32_TN 4
+#endif
+#ifndef PSIM_F32_STAGES
+#define PSIM_F32_STAGES 3
+#endif
+#ifndef PSIM_F32_MINB
+#define PSIM_F32_MINB 2
+#endif
+#ifndef PSIM_F32_VAR
+#define PSIM_F32_VAR 1
+#endif
 template <>
-struct Prod<float> {
-  using C = Cfg<float, 8, 4, 3, 2, 1>;  // 128 x 64, 2 CTAs/SM, scalar FADD
+struct Prod<float> {  // 128 x 64, 2 CTAs/SM, 3 stages, scalar FADD
+  using C = Cfg<float, 8, PSIM_F32_TN, PSIM_F32_STAGES, PSIM_F32_MINB, PSIM_F32_VAR>;
 };
 
 // Edge configurations: 32-row tiles for the last, ragged row tile of a 2-way
