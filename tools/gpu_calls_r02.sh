@@ -284,7 +284,18 @@ z2)
   O=gpurun_out/r02z2; mkdir -p $O
   timeout 900 python bench.py --gpus 2 --config cfg4 --n-v 3000 --steps 1 --warmup 1 --no-cpu --no-e2e > $O/cfg4_n3000_n2.json 2> $O/cfg4_n3000_n2.err
   ;;
+dd)
+  # cfg2 end-to-end breakdown (streamed input, zero-copy values), traced phases
+  O=gpurun_out/r02dd; mkdir -p $O
+  MODES=1 HV=1 REPS=3 NOCLK=1 timeout 900 python tools/exp_e2e.py > $O/exp_e2e.jsonl 2> $O/exp_e2e.err
+  ;;
+ee)
+  # cfg2 streamed kernel: values to HBM (HV=0) vs zero-copy host (HV=1) vs HBM + per-band D2H
+  O=gpurun_out/r02ee; mkdir -p $O
+  MODES=1 HV=0 REPS=3 NOCLK=1 timeout 900 python tools/exp_e2e.py > $O/exp_e2e_hv0.jsonl 2> $O/exp_e2e_hv0.err
+  PSIM_HOST_OUTPUT=bands MODES=1 HV=1 REPS=3 NOCLK=1 timeout 900 python tools/exp_e2e.py > $O/exp_e2e_bands.jsonl 2> $O/exp_e2e_bands.err
+  ;;
 *)
-  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2>"; exit 2
+  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee>"; exit 2
   ;;
 esac
