@@ -295,7 +295,13 @@ ee)
   MODES=1 HV=0 REPS=3 NOCLK=1 timeout 900 python tools/exp_e2e.py > $O/exp_e2e_hv0.jsonl 2> $O/exp_e2e_hv0.err
   PSIM_HOST_OUTPUT=bands MODES=1 HV=1 REPS=3 NOCLK=1 timeout 900 python tools/exp_e2e.py > $O/exp_e2e_bands.jsonl 2> $O/exp_e2e_bands.err
   ;;
+ff)
+  # the streamed kernel's own duration without upload waits (ncu serialises the copy stream first)
+  O=gpurun_out/r02ff; mkdir -p $O
+  MODES=1 HV=1 REPS=1 NOCLK=1 timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,lts__t_sector_hit_rate.pct --clock-control none -k regex:"k_minplus2" --csv --log-file $O/streamed.csv python tools/exp_e2e.py > $O/exp_e2e.jsonl 2> $O/exp_e2e.err
+  timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,lts__t_sector_hit_rate.pct --clock-control none -k regex:"k_minplus2" -c 1 --csv --log-file $O/resident.csv python bench.py --steps 1 --warmup 0 --no-cpu --no-e2e --no-parity > $O/bench.log 2>&1
+  ;;
 *)
-  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee>"; exit 2
+  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff>"; exit 2
   ;;
 esac
