@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(kNT, C::MINB)
     __syncthreads();
     if (!sums_ok) return;
   }
-  const int ty = thread_ty(), tx = thread_tx();
+  const int ty = thread_ty<C::MAP>(), tx = thread_tx<C::MAP>();
   if constexpr (MODE == kCzek2Flat) {
     const int s1 = seg_of(a, col0);
     const int64_t cb = a.seg_c0[s1 + 1];  // first flat column of segment s1 + 1

@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(1024) k_box3_prefix(int64_t i0, int64_t i1, in
 template <typename T, bool RAW>
 static cudaError_t czek3_t(const Czek3Box& b, int64_t* work, int64_t n_single, int64_t n_packed,
                            cudaStream_t st) {
-  using C = typename Prod<T>::C;
+  using C = typename Tile3Cfg<T>::C;
   cudaError_t e = cudaFuncSetAttribute(k_czek3<C, RAW, false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
   if (e == cudaSuccess)
@@ -433,7 +433,7 @@ static cudaError_t czek3_t(const Czek3Box& b, int64_t* work, int64_t n_single, i
 template <typename T>
 static cudaError_t czek3_from_num_t(const Czek3Box& b, int64_t* work, const void* n3, int64_t e0,
                                     int64_t e1, void* vals, cudaStream_t st) {
-  using C = typename Prod<T>::C;
+  using C = typename Tile3Cfg<T>::C;
   if (e1 <= e0) return cudaSuccess;
   const int64_t nJ = b.j1 - b.j0;
   int64_t* op = work + nJ + 1;
@@ -461,11 +461,11 @@ cudaError_t czek3_from_num(int dtype, const Czek3Box& b, int64_t* d_work, const 
 
 void tile_shape(int dtype, int* bm, int* bn) {
   if (dtype == kF64) {
-    *bm = Prod<double>::C::BM;
-    *bn = Prod<double>::C::BN;
+    *bm = Tile3Cfg<double>::C::BM;
+    *bn = Tile3Cfg<double>::C::BN;
   } else {
-    *bm = Prod<float>::C::BM;
-    *bn = Prod<float>::C::BN;
+    *bm = Tile3Cfg<float>::C::BM;
+    *bn = Tile3Cfg<float>::C::BN;
   }
 }
 

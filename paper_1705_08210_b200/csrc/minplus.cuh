@@ -44,13 +44,17 @@ constexpr int kPitchBytes = 144;
 
 // Tile configuration: TM x TN per thread, STAGES-deep cp.async pipeline,
 // MINB CTAs per SM requested from ptxas (__launch_bounds__).
-template <typename T_, int TM_, int TN_, int STAGES_, int MINB_, int VAR_ = 0>
+template <typename T_, int TM_, int TN_, int STAGES_, int MINB_, int VAR_ = 0, int MAP_ = 0>
 struct Cfg {
   using T = T_;
   static constexpr int TM = TM_, TN = TN_, STAGES = STAGES_, MINB = MINB_;
   // FP32 inner-op variant: 0 FMNMX + FADD2, 1 FMNMX + FADD, 2 IMNMX + FADD2,
   // 3 IMNMX + FADD (integer min on the bits: exact for nonnegative floats)
   static constexpr int VAR = VAR_;
+  // thread grid of a warp (thread_ty / thread_tx): 0 = 4 rows x 8 columns
+  // (a warp pair shares its A rows), 1 = 2 rows x 16 columns (measured 0.6%
+  // slower on cfg2, profiles/r02_final/map_ab/; kept for A/B builds)
+  static constexpr int MAP = MAP_;
   static constexpr int BM = 16 * TM;                 // CTA tile rows (W vectors)
   static constexpr int BN = 16 * TN;                 // CTA tile cols (V vectors)
   static constexpr int BK = 128 / (int)sizeof(T);    // q per stage (one 128-B chunk)
@@ -71,9 +75,20 @@ struct Cfg {
 // Production configurations (tile shape of the 2-way and 3-way kernels).
 template <typename T>
 struct Prod;
+#ifndef PSIM_F64_MAP
+#define PSIM_F64_MAP 0
+#endif
 template <>
 struct Prod<double> {
-  using C = Cfg<double, 8, 8, 4, 1, 0>;  // 128 x 128, 1 CTA/SM (254 regs)
+  using C = Cfg<double, 8, 8, 4, 1, 0, PSIM_F64_MAP>;  // 128 x 128, 1 CTA/SM
+};
+
+// 3-way tiles: the production shapes on the 4 x 8 warp grid, which the
+// per-warp pivot rewrite (minplus_tile_pivot_ilv) is written for.
+template <typename T>
+struct Tile3Cfg {
+  using P = typename Prod<T>::C;
+  using C = Cfg<T, P::TM, P::TN, P::STAGES, P::MINB, P::VAR, 0>;
 };
 // (-DPSIM_F32_TN= / _STAGES= / _MINB= / _VAR= override it for A/B builds,
 // tools/build_variant.sh)
@@ -300,10 +315,17 @@ __device__ __forceinline__ void stage_pivot_min(typename C::T* st, const typenam
   }
 }
 
+// Thread (ty, tx) of the 16 x 16 grid: MAP 0 gives each warp 4 rows x 8
+// columns (warps 2p, 2p + 1 share rows), MAP 1 2 rows x 16 columns (every A
+// row read by one warp; a B fetch covers 256 contiguous-pitch bytes).
+template <int MAP = 0>
 __device__ __forceinline__ int thread_ty() {
+  if constexpr (MAP == 1) return (threadIdx.x >> 5) * 2 + ((threadIdx.x & 31) >> 4);
   return ((threadIdx.x >> 5) >> 1) * 4 + ((threadIdx.x & 31) >> 3);
 }
+template <int MAP = 0>
 __device__ __forceinline__ int thread_tx() {
+  if constexpr (MAP == 1) return threadIdx.x & 15;
   return ((threadIdx.x >> 5) & 1) * 8 + (threadIdx.x & 7);
 }
 
@@ -324,7 +346,7 @@ __device__ __forceinline__ void minplus_tile(const typename C::T* __restrict__ W
   using T = typename C::T;
   using V4 = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
   constexpr int S = C::STAGES;
-  const int ty = thread_ty(), tx = thread_tx();
+  const int ty = thread_ty<C::MAP>(), tx = thread_tx<C::MAP>();
   T vs = T();
 #pragma unroll
   for (int m = 0; m < C::TM; ++m)
@@ -488,7 +510,7 @@ __device__ __forceinline__ void minplus_tile_tma(const void* mapW, int w_row0, c
   };
   if (tid == 0)
     for (int kt = 0; kt < S && kt < KT; ++kt) issue(kt);
-  const int ty = thread_ty(), tx = thread_tx();
+  const int ty = thread_ty<C::MAP>(), tx = thread_tx<C::MAP>();
   for (int kt = 0; kt < KT; ++kt) {
     const int s = kt % S;
     const unsigned ph = (unsigned)(kt / S) & 1u;
@@ -532,6 +554,7 @@ __device__ __forceinline__ void minplus_tile_pivot_ilv(const void* mapA, int a_r
   using V4 = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
   static_assert(C::BK / C::VEC == C::TM, "one chunk of the warp's rows per micro-step");
   static_assert(A >= 1 && A < C::STAGES, "transform distance");
+  static_assert(C::MAP == 0, "the per-warp rewrite follows the 4 x 8 warp grid");
   constexpr int S = C::STAGES;
   constexpr int XS = (C::BM + C::BN) * C::PITCH;  // pivot slot inside a stage
   constexpr unsigned kBytes = (C::BM + C::BN + 1) * C::PITCH * sizeof(T);

@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kNT, sizeof(T) == 8 ? 1 : 2)
   for (int m = 0; m < C::TM; ++m)
 #pragma unroll
     for (int n = 0; n < C::TN; ++n) acc[m][n] = T(0);
-  const int ty = thread_ty(), tx = thread_tx();
+  const int ty = thread_ty<C::MAP>(), tx = thread_tx<C::MAP>();
   __syncthreads();
   const long long c0 = clock64();
   for (int64_t it = 0; it < iters; ++it) {

@@ -5,12 +5,9 @@
 set -e
 cd "$(dirname "$0")/.."
 name=$1; shift
-out=build/ab/$name; mkdir -p $out/obj
-for src in paper_1705_08210_b200/csrc/*.cu; do
-  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
-    -Iinclude -Ipaper_1705_08210_b200/csrc "$@" -c $src -o $out/obj/$(basename $src .cu).o &
-done
-wait
-ls $out/obj/*.o > /dev/null
+out=build/ab/$name; rm -rf $out; mkdir -p $out/obj
+ls paper_1705_08210_b200/csrc/*.cu | xargs -P 8 -I{} sh -c \
+  'nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
+     -Iinclude -Ipaper_1705_08210_b200/csrc '"$*"' -c {} -o '"$out"'/obj/$(basename {} .cu).o'
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/libpsim.so $out/obj/*.o
 echo $out/libpsim.so

@@ -301,7 +301,17 @@ ff)
   MODES=1 HV=1 REPS=1 NOCLK=1 timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,lts__t_sector_hit_rate.pct --clock-control none -k regex:"k_minplus2" --csv --log-file $O/streamed.csv python tools/exp_e2e.py > $O/exp_e2e.jsonl 2> $O/exp_e2e.err
   timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,lts__t_sector_hit_rate.pct --clock-control none -k regex:"k_minplus2" -c 1 --csv --log-file $O/resident.csv python bench.py --steps 1 --warmup 0 --no-cpu --no-e2e --no-parity > $O/bench.log 2>&1
   ;;
+gg)
+  # FP64 2-way warp grid A/B: 4 x 8 (product) vs 2 x 16 (tools/build_variant.sh f64_map1 -DPSIM_F64_MAP=1)
+  O=gpurun_out/r02gg; mkdir -p $O
+  B="python bench.py --steps 3 --warmup 1 --no-cpu --no-e2e"
+  for r in 1 2; do
+    timeout 600 $B > $O/map0_$r.json 2> $O/map0_$r.err
+    PSIM_LIB=build/ab/f64_map1/libpsim.so timeout 600 $B > $O/map1_$r.json 2> $O/map1_$r.err
+  done
+  PSIM_LIB=build/ab/f64_map1/libpsim.so timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $O/pytest_map1.log 2>&1; echo "rc=$?" >> $O/pytest_map1.log
+  ;;
 *)
-  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff>"; exit 2
+  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg>"; exit 2
   ;;
 esac
