@@ -75,20 +75,38 @@ struct Cfg {
 // Production configurations (tile shape of the 2-way and 3-way kernels).
 template <typename T>
 struct Prod;
+// (-DPSIM_F64_TN= / _STAGES= / _MINB= / _MAP= override it for A/B builds,
+// tools/build_variant.sh)
+#ifndef PSIM_F64_TN
+#define PSIM_F64_TN 8
+#endif
+#ifndef PSIM_F64_STAGES
+#define PSIM_F64_STAGES 4
+#endif
+#ifndef PSIM_F64_MINB
+#define PSIM_F64_MINB 1
+#endif
 #ifndef PSIM_F64_MAP
 #define PSIM_F64_MAP 0
 #endif
 template <>
-struct Prod<double> {
-  using C = Cfg<double, 8, 8, 4, 1, 0, PSIM_F64_MAP>;  // 128 x 128, 1 CTA/SM
+struct Prod<double> {  // 128 x 128, 1 CTA/SM, 4 stages
+  using C = Cfg<double, 8, PSIM_F64_TN, PSIM_F64_STAGES, PSIM_F64_MINB, 0, PSIM_F64_MAP>;
 };
 
-// 3-way tiles: the production shapes on the 4 x 8 warp grid, which the
-// per-warp pivot rewrite (minplus_tile_pivot_ilv) is written for.
+// 3-way tiles (k_czek3; psim_tile_shape reports their shape): 128 x 128 FP64
+// / 128 x 64 FP32 on the 4 x 8 warp grid, which the per-warp pivot rewrite
+// (minplus_tile_pivot_ilv) is written for. Fixed, so 2-way A/B builds leave
+// the 3-way kernels alone.
 template <typename T>
-struct Tile3Cfg {
-  using P = typename Prod<T>::C;
-  using C = Cfg<T, P::TM, P::TN, P::STAGES, P::MINB, P::VAR, 0>;
+struct Tile3Cfg;
+template <>
+struct Tile3Cfg<double> {
+  using C = Cfg<double, 8, 8, 4, 1, 0, 0>;
+};
+template <>
+struct Tile3Cfg<float> {
+  using C = Cfg<float, 8, 4, 3, 2, 1, 0>;
 };
 // (-DPSIM_F32_TN= / _STAGES= / _MINB= / _VAR= override it for A/B builds,
 // tools/build_variant.sh)

@@ -311,7 +311,18 @@ gg)
   done
   PSIM_LIB=build/ab/f64_map1/libpsim.so timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $O/pytest_map1.log 2>&1; echo "rc=$?" >> $O/pytest_map1.log
   ;;
+hh)
+  # FP64 2-way tile A/B on cfg2 with TMA staging: 8x8 4-stage (product) vs 8x4 2 CTAs/SM (4 / 3 stages), 8x8 5-stage
+  O=gpurun_out/r02hh; mkdir -p $O
+  B="python bench.py --steps 3 --warmup 1 --no-cpu --no-e2e"
+  for r in 1 2; do
+    timeout 600 $B > $O/prod_$r.json 2> $O/prod_$r.err
+    for v in f64_8x4_s4 f64_8x4_s3 f64_8x8_s5; do
+      PSIM_LIB=build/ab/$v/libpsim.so timeout 600 $B > $O/${v}_$r.json 2> $O/${v}_$r.err
+    done
+  done
+  ;;
 *)
-  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg>"; exit 2
+  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh>"; exit 2
   ;;
 esac
