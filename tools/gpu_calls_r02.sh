@@ -322,7 +322,16 @@ hh)
     done
   done
   ;;
+final4)
+  # round-end check on 4 GPUs: GPU suite (NCCL world 2 / 4), cfg2 at N = 2 / 4 as the driver runs it
+  O=gpurun_out/r02final4; mkdir -p $O
+  nvidia-smi topo -m > $O/topo.txt 2>&1
+  timeout 1800 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
+  timeout 900 python bench.py --gpus 2 --steps 5 --warmup 3 > $O/bench_cfg2_n2.json 2> $O/bench_cfg2_n2.err
+  timeout 900 python bench.py --gpus 4 --steps 5 --warmup 3 > $O/bench_cfg2_n4.json 2> $O/bench_cfg2_n4.err
+  timeout 900 python bench.py --gpus 4 --impl reference --steps 2 --warmup 1 > $O/bench_ref_n4.json 2> $O/bench_ref_n4.err
+  ;;
 *)
-  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh>"; exit 2
+  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh final4>"; exit 2
   ;;
 esac
