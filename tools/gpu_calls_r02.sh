@@ -331,7 +331,18 @@ final4)
   timeout 900 python bench.py --gpus 4 --steps 5 --warmup 3 > $O/bench_cfg2_n4.json 2> $O/bench_cfg2_n4.err
   timeout 900 python bench.py --gpus 4 --impl reference --steps 2 --warmup 1 > $O/bench_ref_n4.json 2> $O/bench_ref_n4.err
   ;;
+ii)
+  # FP32 2-way micro-step unroll A/B at cfg3's n_f with TMA staging (product 4 vs 8 / 2)
+  O=gpurun_out/r02ii; mkdir -p $O
+  B="python bench.py --config cfg3 --n-v 100000 --steps 2 --warmup 1 --no-cpu --no-e2e --no-parity"
+  for r in 1 2; do
+    timeout 600 $B > $O/prod_$r.json 2> $O/prod_$r.err
+    for v in kku8 kku2; do
+      PSIM_LIB=build/ab/$v/libpsim.so timeout 600 $B > $O/${v}_$r.json 2> $O/${v}_$r.err
+    done
+  done
+  ;;
 *)
-  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh final4>"; exit 2
+  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh final4 ii>"; exit 2
   ;;
 esac
