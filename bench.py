@@ -404,7 +404,11 @@ def run_ours(args) -> dict | None:
         if e2e:
             line["e2e"] = e2e
         if not args.no_cpu:
-            line["cpu_baseline"] = cpu_baseline(arity, precision, n_f, bits)
+            try:
+                line["cpu_baseline"] = cpu_baseline(arity, precision, n_f, bits)
+            except Exception as e:  # noqa: BLE001 -- reported in the line
+                line["cpu_baseline"] = {"error": f"{type(e).__name__}: {e}"}
+                log(f"[bench] cpu baseline failed: {e}")
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -500,6 +504,31 @@ class RuntimeBench:
 
 
 def sampled_parity(runner, prob, bits, world, dev) -> dict:
+    """Checker, run after the timed region (see _local_parity). A checker that
+    raises is reported in the line ("checker_errors", "how") instead of
+    ending the bench, and every rank still joins the sum over ranks."""
+    import torch
+
+    try:
+        sampled, mismatches, how = _local_parity(runner, prob, bits)
+        errors = 0
+    except Exception as e:  # noqa: BLE001 -- reported, not swallowed
+        sampled, mismatches, errors = 0, 0, 1
+        how = f"checker failed on rank {os.environ.get('RANK', '0')}: {type(e).__name__}: {e}"
+        log(f"[bench] parity checker failed: {how}")
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([sampled, mismatches, errors], dtype=torch.int64, device=dev)
+        dist.all_reduce(t)
+        sampled, mismatches, errors = (int(x) for x in t.tolist())
+    out = {"sampled": sampled, "mismatches": mismatches, "bitwise": True, "how": how}
+    if errors:
+        out["checker_errors"] = errors
+    return out
+
+
+def _local_parity(runner, prob, bits) -> tuple:
     """Checker, run after the timed region: tuples of the benchmarked run
     recomputed from their own columns by the oracle (SURVEY 8d "Parity at
     full size": pair_numerators / column_sums / metric2_value, or the 3-way
@@ -507,8 +536,8 @@ def sampled_parity(runner, prob, bits, world, dev) -> dict:
     wrote. 2-way: per value piece of this rank, a grid of sampled rows x
     sampled columns (so ~10^4 pairs need only a few hundred generated
     columns); 3-way: ~10^4 triples (20 pivots x a 25 x 25 grid) of the
-    last pivot chunk. Mismatches and
-    sample counts are summed over ranks."""
+    last pivot chunk (at N > 1: the last box in each rank's runtime scratch).
+    Returns this rank's (sampled, mismatches, how)."""
     import torch
 
     from oracle import propsim_np as O
@@ -593,15 +622,9 @@ def sampled_parity(runner, prob, bits, world, dev) -> dict:
             sampled += len(got)
         how = (f"{len(js)} pivots of the last pivot chunk x (sampled rows x sampled columns), "
                "recomputed from their columns by oracle.propsim_np.triple_values_grid")
-    else:  # (still joins the sum over ranks below: other ranks may hold values)
-        how = "values not retained by this harness on rank 0"
-    if world > 1:
-        import torch.distributed as dist
-
-        t = torch.tensor([sampled, mismatches], dtype=torch.int64, device=dev)
-        dist.all_reduce(t)
-        sampled, mismatches = int(t[0].item()), int(t[1].item())
-    return {"sampled": sampled, "mismatches": mismatches, "bitwise": True, "how": how}
+    else:  # (still joins the sum over ranks: other ranks may hold values)
+        how = "values not retained by this harness on this rank"
+    return sampled, mismatches, how
 
 
 def e2e_2way(P, prob, grid, precision, args, total_cmp, world, rank) -> dict:
