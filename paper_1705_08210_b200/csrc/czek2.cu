@@ -179,28 +179,51 @@ __device__ __forceinline__ int64_t streamed_tile(const Args2<T>& a) {
 }
 
 // Column sums of the 128 (BM) vectors of row tile r, each a sequential
-// ascending-q fold from +0 (k_colsum's order), staged 32 fields at a time
-// through shared memory with coalesced loads; published with sum_ready[r].
+// ascending-q fold from +0 (k_colsum's order), staged kSumQ fields at a time
+// through double-buffered shared memory with coalesced loads: the loads of
+// the next chunk are in flight (registers) while the current one is folded,
+// one barrier per chunk. Published with sum_ready[r].
 template <class C>
 __device__ void streamed_row_sums(const Args2<typename C::T>& a, int64_t r,
                                   typename C::T* smem) {
   using T = typename C::T;
+  constexpr int kSumQ = 64;                 // fields per chunk
+  constexpr int kPitch = kSumQ + 1;         // conflict-free column reads
+  constexpr int kRows = C::BM / (kNT / 32);  // rows each warp stages
+  constexpr int kPer = kSumQ / 32;          // fields per lane per row
+  static_assert(2 * C::BM * kPitch * (int)sizeof(T) <= C::SMEM_BYTES, "sum staging");
   const int64_t v0 = r * C::BM;
   const int nv = (int)min64(C::BM, a.n - v0);
   if (!cta_wait_ready(a.ready + v0 / a.chunk, 0)) return;  // aborted: sums never published
-  T (*tile)[33] = reinterpret_cast<T (*)[33]>(smem);  // [BM][33]
+  T (*tile)[C::BM][kPitch] = reinterpret_cast<T (*)[C::BM][kPitch]>(smem);  // [2][BM][pitch]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  T acc = T(0);
-  for (int64_t q0 = 0; q0 < a.n_f; q0 += 32) {
-    const int64_t q = q0 + lane;
-    for (int lv = warp; lv < C::BM; lv += kNT / 32)
-      tile[lv][lane] = (lv < nv && q < a.n_f) ? __ldcg(a.W + (v0 + lv) * a.ldw + q) : T(0);
-    __syncthreads();
-    if (threadIdx.x < C::BM) {
-      const int cnt = (int)min64(32, a.n_f - q0);
-      for (int k = 0; k < cnt; ++k) acc = Traits<T>::add(acc, tile[threadIdx.x][k]);
+  T nxt[kRows][kPer];
+  auto load = [&](int64_t q0) {
+#pragma unroll
+    for (int j = 0; j < kRows; ++j) {
+      const int lv = warp + j * (kNT / 32);
+#pragma unroll
+      for (int h = 0; h < kPer; ++h) {
+        const int64_t q = q0 + h * 32 + lane;
+        nxt[j][h] = (lv < nv && q < a.n_f) ? __ldcg(a.W + (v0 + lv) * a.ldw + q) : T(0);
+      }
     }
+  };
+  T acc = T(0);
+  load(0);
+  int buf = 0;
+  for (int64_t q0 = 0; q0 < a.n_f; q0 += kSumQ, buf ^= 1) {
+#pragma unroll
+    for (int j = 0; j < kRows; ++j)
+#pragma unroll
+      for (int h = 0; h < kPer; ++h) tile[buf][warp + j * (kNT / 32)][h * 32 + lane] = nxt[j][h];
+    // (this chunk's buffer was last read two chunks ago, before the previous barrier)
     __syncthreads();
+    if (q0 + kSumQ < a.n_f) load(q0 + kSumQ);
+    if (threadIdx.x < C::BM) {
+      const int cnt = (int)min64(kSumQ, a.n_f - q0);
+      for (int k = 0; k < cnt; ++k) acc = Traits<T>::add(acc, tile[buf][threadIdx.x][k]);
+    }
   }
   if (threadIdx.x < nv) a.sums[v0 + threadIdx.x] = acc;
   __syncthreads();

@@ -664,7 +664,7 @@ struct Run2 : Rank {
     if (streamed) {
       int bm = 0, bn = 0;
       psim::tile_shape(dtype, &bm, &bn);
-      chunk = std::max<int64_t>(256, (n_vp + 63) / 64);
+      chunk = std::max<int64_t>(64, (n_vp + 255) / 256);  // <= 256 chunks (engine2.stream_chunk)
       ready = static_cast<unsigned*>(A.take(((n_vp + chunk - 1) / chunk + (n_vp + bm - 1) / bm) * 4));
       scratch_sums = A.take(n_vp * esz);
     }

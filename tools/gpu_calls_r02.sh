@@ -342,7 +342,20 @@ ii)
     done
   done
   ;;
+jj)
+  # streamed kernel: 64 / 1 / 256 upload chunks (tools/exp_stream_order.py)
+  O=gpurun_out/r02jj; mkdir -p $O
+  timeout 900 python tools/exp_stream_order.py > $O/exp_stream_order.jsonl 2> $O/exp_stream_order.err
+  ;;
+kk)
+  # streamed column-sum CTAs: prefetching double-buffered fold (product build) vs the round-1 fold
+  # (build/ab/sums_v1), streamed kernel speed with 1 / 64 upload chunks; streamed GPU tests
+  O=gpurun_out/r02kk; mkdir -p $O
+  timeout 900 python tools/exp_stream_order.py > $O/new.jsonl 2> $O/new.err
+  PSIM_LIB=build/ab/sums_v1/libpsim.so timeout 900 python tools/exp_stream_order.py > $O/old.jsonl 2> $O/old.err
+  timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "stream or e2e or host or pageable" > $O/pytest_stream.log 2>&1; echo "rc=$?" >> $O/pytest_stream.log
+  ;;
 *)
-  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh final4 ii>"; exit 2
+  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh final4 ii jj kk>"; exit 2
   ;;
 esac
