@@ -355,7 +355,18 @@ kk)
   PSIM_LIB=build/ab/sums_v1/libpsim.so timeout 900 python tools/exp_stream_order.py > $O/old.jsonl 2> $O/old.err
   timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "stream or e2e or host or pageable" > $O/pytest_stream.log 2>&1; echo "rc=$?" >> $O/pytest_stream.log
   ;;
+final1)
+  # round-end check on 1 GPU: GPU suite, smoke, default bench (all legs), reference arm, cfg4 line,
+  # launch list of the default bench command
+  O=gpurun_out/r02final1; mkdir -p $O
+  timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "rc=$?" >> $O/smoke.log
+  timeout 900 python bench.py > $O/bench_cfg2.json 2> $O/bench_cfg2.err
+  timeout 900 python bench.py --impl reference > $O/bench_ref.json 2> $O/bench_ref.err
+  timeout 900 python bench.py --config cfg4 --steps 2 --warmup 3 > $O/bench_cfg4.json 2> $O/bench_cfg4.err
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_cfg2.csv python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e > $O/ncu_launches.log 2>&1
+  ;;
 *)
-  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh final4 ii jj kk>"; exit 2
+  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh final4 ii jj kk final1>"; exit 2
   ;;
 esac
