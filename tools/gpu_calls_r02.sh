@@ -366,7 +366,13 @@ final1)
   timeout 900 python bench.py --config cfg4 --steps 2 --warmup 3 > $O/bench_cfg4.json 2> $O/bench_cfg4.err
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_cfg2.csv python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e > $O/ncu_launches.log 2>&1
   ;;
+final2)
+  # 2 GPUs after the streamed-upload change: runtime / NCCL tests, cfg2 N=2 with its e2e legs
+  O=gpurun_out/r02final2; mkdir -p $O
+  timeout 900 python -m pytest tests/test_gpu_runtime.py tests/test_gpu_nccl.py -x -q -p no:cacheprovider > $O/pytest_rt.log 2>&1; echo "rc=$?" >> $O/pytest_rt.log
+  timeout 900 python bench.py --gpus 2 --steps 5 --warmup 3 > $O/bench_cfg2_n2.json 2> $O/bench_cfg2_n2.err
+  ;;
 *)
-  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh final4 ii jj kk final1>"; exit 2
+  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh final4 ii jj kk final1 final2>"; exit 2
   ;;
 esac
