@@ -372,7 +372,12 @@ final2)
   timeout 900 python -m pytest tests/test_gpu_runtime.py tests/test_gpu_nccl.py -x -q -p no:cacheprovider > $O/pytest_rt.log 2>&1; echo "rc=$?" >> $O/pytest_rt.log
   timeout 900 python bench.py --gpus 2 --steps 5 --warmup 3 > $O/bench_cfg2_n2.json 2> $O/bench_cfg2_n2.err
   ;;
+ll)
+  # cfg2 on one GPU under the circulant plans n_pv = 1/2/4/8 (decomposition cost with the TMA kernels)
+  O=gpurun_out/r02ll; mkdir -p $O
+  timeout 900 python tools/exp_local_grids.py > $O/local_grids.jsonl 2> $O/local_grids.err
+  ;;
 *)
-  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh final4 ii jj kk final1 final2>"; exit 2
+  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh final4 ii jj kk final1 final2 ll>"; exit 2
   ;;
 esac
