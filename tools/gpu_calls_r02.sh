@@ -377,7 +377,24 @@ ll)
   O=gpurun_out/r02ll; mkdir -p $O
   timeout 900 python tools/exp_local_grids.py > $O/local_grids.jsonl 2> $O/local_grids.err
   ;;
+mm)
+  # ncu --set full of the round-end 3-way single-pivot kernel (interleaved pivot loop + single-pivot
+  # epilogue) at a cfg4-shaped box, summarised on the box
+  O=gpurun_out/r02mm; mkdir -p $O
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_czek3" -s 0 -c 1 -o $O/czek3_final python bench.py --config cfg4 --n-v 1536 --steps 1 --warmup 1 --no-cpu --no-e2e --no-parity > $O/ncu_3.log 2>&1
+  python tools/ncu_summary.py $O/czek3_final.ncu-rep "k_czek3 single-pivot grid, round-end tree, cfg4 n_f=10000, n_v=1536" > $O/ncu_czek3_final.md 2>&1
+  ncu -i $O/czek3_final.ncu-rep --page source --csv --print-source sass > $O/czek3_src.csv 2>/dev/null
+  python tools/ncu_stalls.py $O/czek3_src.csv > $O/czek3_stalls.txt 2>&1
+  rm -f $O/czek3_src.csv
+  du -sm $O; if [ $(du -sm $O | cut -f1) -gt 55 ]; then rm -f $O/*.ncu-rep; fi
+  ;;
+scale4)
+  # round-end cfg3 / cfg5 on 4 GPUs
+  O=gpurun_out/r02scale4; mkdir -p $O
+  timeout 1500 python bench.py --gpus 4 --config cfg3 --steps 2 --warmup 3 --no-cpu > $O/bench_cfg3_n4.json 2> $O/bench_cfg3_n4.err
+  timeout 1500 python bench.py --gpus 4 --config cfg5 --steps 2 --warmup 3 --no-cpu > $O/bench_cfg5_n4.json 2> $O/bench_cfg5_n4.err
+  ;;
 *)
-  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh final4 ii jj kk final1 final2 ll>"; exit 2
+  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh final4 ii jj kk final1 final2 ll mm scale4>"; exit 2
   ;;
 esac
