@@ -339,7 +339,11 @@ def run_ours(args) -> dict | None:
     # end-to-end through the public API with host buffers
     e2e = None
     runner.teardown()
-    if not args.no_e2e and arity == 2:
+    skip = None if args.no_e2e else e2e_host_shortfall(prob, grid, world)
+    if skip:
+        e2e = {"skipped": skip}
+        log(f"[bench] e2e skipped: {skip}")
+    elif not args.no_e2e and arity == 2:
         e2e = e2e_2way(P, prob, grid, precision, args, total_cmp, world, rank)
     elif not args.no_e2e and arity == 3:
         e2e = e2e_3way(P, prob, grid, precision, args, total_cmp, world, rank)
@@ -625,6 +629,28 @@ def _local_parity(runner, prob, bits) -> tuple:
     else:  # (still joins the sum over ranks: other ranks may hold values)
         how = "values not retained by this harness on this rank"
     return sampled, mismatches, how
+
+
+def e2e_host_shortfall(prob, grid, world) -> str | None:
+    """The e2e legs pin every rank's input slab (and, 2-way, its values) in
+    host memory. None when that fits in min(half the host's available
+    memory, 256 GB) across the ranks of this node, else the reason to skip
+    them: cfg5 at N = 4 would pin 4 x 80 GB, and on the B200 box that got
+    its ranks killed by the host (profiles/r02_final/scale4/); cfg3 at N = 4
+    pins 120 GB and runs. Decided from node-wide numbers, so all ranks of a
+    node skip together."""
+    import psutil
+
+    esz = 8 if prob.precision == "double" else 4
+    n_fp, n_vp = prob.n_f // grid.n_pf, prob.n_v // grid.n_pv
+    tuples = math.comb(prob.n_v, prob.arity)
+    per_rank = n_fp * n_vp * esz + (tuples * esz // world if prob.arity == 2 else 0)
+    local = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    limit = min(psutil.virtual_memory().available // 2, 256 << 30)
+    if per_rank * local > limit:
+        return (f"pinned host buffers {per_rank * local / 1e9:.0f} GB on this node > "
+                f"{limit / 1e9:.0f} GB (min of half the available memory and 256 GiB)")
+    return None
 
 
 def e2e_2way(P, prob, grid, precision, args, total_cmp, world, rank) -> dict:

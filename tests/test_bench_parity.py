@@ -78,3 +78,17 @@ def test_checker_failure_is_reported_not_raised():
     prob = Problem(2, N_F, 60, gen_random_exact(bench.SEED, N_F, 60, BITS), "double")
     got = bench.sampled_parity(Broken(), prob, BITS, 1, None)
     assert got["checker_errors"] == 1 and "no values" in got["how"]
+
+
+def test_e2e_legs_skip_when_pinned_buffers_exceed_host_memory():
+    """cfg5 at N = 4 would pin 4 x 80 GB of input (its ranks were killed by the
+    host on the B200 box): the bench reports the e2e leg as skipped instead;
+    cfg2 at N = 1 pins 12.8 GB and runs."""
+    from paper_1705_08210_b200 import DecompGrid
+
+    a, prec, nf, nv, bits, _ = bench.CONFIGS["cfg5"]
+    p5 = Problem(a, nf, nv, gen_random_exact(bench.SEED, nf, nv, bits), prec)
+    assert "pinned host buffers" in bench.e2e_host_shortfall(p5, DecompGrid(n_pf=4), 4)
+    a, prec, nf, nv, bits, _ = bench.CONFIGS["cfg2"]
+    p2 = Problem(a, nf, nv, gen_random_exact(bench.SEED, nf, nv, bits), prec)
+    assert bench.e2e_host_shortfall(p2, DecompGrid(), 1) is None
