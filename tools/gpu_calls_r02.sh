@@ -395,7 +395,13 @@ scale4)
   timeout 1500 python bench.py --gpus 4 --config cfg5 --steps 2 --warmup 3 --no-cpu > $O/bench_cfg5_n4.json 2> $O/bench_cfg5_n4.err
   # (the first run of this call had no e2e guard: the cfg5 e2e leg pinned 4 x 80 GB and the host killed the ranks)
   ;;
+cfg5n4)
+  # cfg5 on 4 GPUs with the e2e host-memory guard
+  O=gpurun_out/r02cfg5; mkdir -p $O
+  free -g > $O/free.txt
+  timeout 1500 python bench.py --gpus 4 --config cfg5 --steps 2 --warmup 3 --no-cpu > $O/bench_cfg5_n4.json 2> $O/bench_cfg5_n4.err
+  ;;
 *)
-  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh final4 ii jj kk final1 final2 ll mm scale4>"; exit 2
+  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh final4 ii jj kk final1 final2 ll mm scale4 cfg5n4>"; exit 2
   ;;
 esac
