@@ -561,8 +561,9 @@ def _local_parity(runner, prob, bits) -> tuple:
         n_pf = getattr(getattr(runner, "grid", None), "n_pf", 1)
         # sampled rows x sampled columns per piece; the recompute costs
         # ~side^2 * n_f adds, so side shrinks with the field depth (cfg2:
-        # 160 x 160 -> ~1.2e4 pairs of the diagonal piece; cfg5: ~17 x 17)
-        side = int(math.sqrt(6e8 / n_f / max(1, len(pieces))))
+        # 160 x 160 -> ~1.3e4 pairs of the diagonal piece; cfg5 at N = 4: ~63 x 63
+        # per rank, ~25 s of numpy on each rank)
+        side = int(math.sqrt(8e9 / n_f / max(1, len(pieces))))
         side = max(8, min(160, side))
         for pc in pieces:
             if pc.values is None or pc.r1 <= pc.r0:
