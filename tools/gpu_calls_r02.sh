@@ -401,7 +401,13 @@ cfg5n4)
   free -g > $O/free.txt
   timeout 1500 python bench.py --gpus 4 --config cfg5 --steps 2 --warmup 3 --no-cpu > $O/bench_cfg5_n4.json 2> $O/bench_cfg5_n4.err
   ;;
+par4)
+  # 4 GPUs: cfg5 / cfg3 with the larger sampled-parity budget
+  O=gpurun_out/r02par4; mkdir -p $O
+  timeout 1800 python bench.py --gpus 4 --config cfg5 --steps 2 --warmup 3 --no-cpu > $O/bench_cfg5_n4.json 2> $O/bench_cfg5_n4.err
+  timeout 1800 python bench.py --gpus 4 --config cfg3 --steps 2 --warmup 3 --no-cpu > $O/bench_cfg3_n4.json 2> $O/bench_cfg3_n4.err
+  ;;
 *)
-  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh final4 ii jj kk final1 final2 ll mm scale4 cfg5n4>"; exit 2
+  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh final4 ii jj kk final1 final2 ll mm scale4 cfg5n4 par4>"; exit 2
   ;;
 esac
