@@ -407,7 +407,14 @@ par4)
   timeout 1800 python bench.py --gpus 4 --config cfg5 --steps 2 --warmup 3 --no-cpu > $O/bench_cfg5_n4.json 2> $O/bench_cfg5_n4.err
   timeout 1800 python bench.py --gpus 4 --config cfg3 --steps 2 --warmup 3 --no-cpu > $O/bench_cfg3_n4.json 2> $O/bench_cfg3_n4.err
   ;;
+f32ncu)
+  # ncu --set full (with source) of the FP32 2-way kernel: where the smem bank-conflict counter comes from
+  O=gpurun_out/r02f32ncu; mkdir -p $O
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_minplus2" -s 0 -c 1 -o $O/f32 python bench.py --config cfg3 --n-v 16384 --steps 1 --warmup 1 --no-cpu --no-e2e --no-parity > $O/ncu.log 2>&1
+  python tools/ncu_summary.py $O/f32.ncu-rep "k_minplus2 FP32 (cfg3 n_f, n_v=16384), round-end tree" > $O/ncu_f32.md 2>&1
+  du -sm $O; if [ $(du -sm $O | cut -f1) -gt 55 ]; then rm -f $O/*.ncu-rep; fi
+  ;;
 *)
-  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh final4 ii jj kk final1 final2 ll mm scale4 cfg5n4 par4>"; exit 2
+  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh final4 ii jj kk final1 final2 ll mm scale4 cfg5n4 par4 f32ncu>"; exit 2
   ;;
 esac
