@@ -414,7 +414,14 @@ f32ncu)
   python tools/ncu_summary.py $O/f32.ncu-rep "k_minplus2 FP32 (cfg3 n_f, n_v=16384), round-end tree" > $O/ncu_f32.md 2>&1
   du -sm $O; if [ $(du -sm $O | cut -f1) -gt 55 ]; then rm -f $O/*.ncu-rep; fi
   ;;
+final1b)
+  # last 1-GPU check after the bench changes: GPU suite, smoke, default bench
+  O=gpurun_out/r02final1b; mkdir -p $O
+  timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "rc=$?" >> $O/smoke.log
+  timeout 900 python bench.py > $O/bench_cfg2.json 2> $O/bench_cfg2.err
+  ;;
 *)
-  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh final4 ii jj kk final1 final2 ll mm scale4 cfg5n4 par4 f32ncu>"; exit 2
+  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh final4 ii jj kk final1 final2 ll mm scale4 cfg5n4 par4 f32ncu final1b>"; exit 2
   ;;
 esac
