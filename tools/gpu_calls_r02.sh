@@ -421,7 +421,13 @@ final1b)
   timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "rc=$?" >> $O/smoke.log
   timeout 900 python bench.py > $O/bench_cfg2.json 2> $O/bench_cfg2.err
   ;;
+cfg4n24)
+  # round-end cfg4 at N = 2 / 4 with the 3-way sampled parity from the runtime scratch boxes
+  O=gpurun_out/r02cfg4; mkdir -p $O
+  timeout 1500 python bench.py --gpus 4 --config cfg4 --steps 2 --warmup 3 --no-cpu > $O/bench_cfg4_n4.json 2> $O/bench_cfg4_n4.err
+  timeout 1500 python bench.py --gpus 2 --config cfg4 --steps 2 --warmup 3 --no-cpu > $O/bench_cfg4_n2.json 2> $O/bench_cfg4_n2.err
+  ;;
 *)
-  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh final4 ii jj kk final1 final2 ll mm scale4 cfg5n4 par4 f32ncu final1b>"; exit 2
+  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh final4 ii jj kk final1 final2 ll mm scale4 cfg5n4 par4 f32ncu final1b cfg4n24>"; exit 2
   ;;
 esac
