@@ -288,7 +288,7 @@ __device__ __forceinline__ void tile_gen(const void* mapA, int a_row0, const voi
 // compute of stage kt: micro-step u loads chunk u of the warp's rows at its top
 // and stores min(x, chunk) at its bottom, so the load latency hides behind the
 // micro-step's 512 FP instructions
-template <class Cc, int A>
+template <class Cc, int A, bool PAIR = false>
 __device__ __forceinline__ void tile_ilv(const void* mapA, int a_row0, const void* mapC,
                                          int c_row0, const void* mapB, int p_row, int64_t n_f,
                                          double (&acc)[Cc::TM][Cc::TN], double* smem) {
@@ -347,16 +347,22 @@ __device__ __forceinline__ void tile_ilv(const void* mapA, int a_row0, const voi
     for (int u = 0; u < Cc::TM; ++u) {
       double2* pa = reinterpret_cast<double2*>(nx + roff + 16 * u * Cc::PITCH);
       double2 a;
-      if (xf) a = *pa;
+      // PAIR: the two warps of a pair read the same rows; each rewrites half
+      const bool mine = xf && (!PAIR || (u & 1) == (w & 1));
+      if (mine) a = *pa;
       micro_step<Cc>(acc, st, st + Cc::BM * Cc::PITCH, ty, tx, u * Cc::VEC);
-      if (xf) {
+      if (mine) {
         a.x = Traits<double>::min(x.x, a.x);
         a.y = Traits<double>::min(x.y, a.y);
         *pa = a;
       }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncwarp();
+    if (PAIR) {  // the partner's half of stage kt + A before either computes it
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + (w >> 1)) : "memory");
+    } else {
+      __syncwarp();
+    }
     if (lane == 0) mbar_arrive(&empty[s]);
     if (tid == 0 && kt + S < KT) {
       mbar_wait(&empty[s], ph);
@@ -485,9 +491,10 @@ using CS = Cfg<double, 8, 8, S, 1, 0>;
 //    6 own A2 S6, 7 prod S6, 8 tma2 S6; gen (production loop with knobs), S6:
 //    9 D3, 10 D2 box but no transform, 11 D2 no fence, 12 D2 no box / transform
 //    (ready barriers only), 13 D4; ilv: 14 A1 S4, 15 A1 S5, 16 A1 S6, 17 A2 S6;
-//    w16 mapping, S4: 18 2-way (no pivot), 19 ilv A1
-constexpr int kVars = 20;
-constexpr int kStagesOf[kVars] = {4, 4, 4, 4, 5, 6, 6, 6, 6, 6, 6, 6, 6, 6, 4, 5, 6, 6, 4, 4};
+//    w16 mapping, S4: 18 2-way (no pivot), 19 ilv A1; 20 ilv A1 S4 with the rewrite split
+//    between the warps of a pair (named barrier per stage)
+constexpr int kVars = 21;
+constexpr int kStagesOf[kVars] = {4, 4, 4, 4, 5, 6, 6, 6, 6, 6, 6, 6, 6, 6, 4, 5, 6, 6, 4, 4, 4};
 
 template <int V>
 __global__ void __launch_bounds__(kNT, 1)
@@ -500,7 +507,9 @@ __global__ void __launch_bounds__(kNT, 1)
   const int64_t row0 = bi * Cc::BM, col0 = bj * Cc::BN;
   const int p = (int)pivot_of(bi, bj, n);
   double acc[Cc::TM][Cc::TN];
-  if constexpr (V == 18 || V == 19) {
+  if constexpr (V == 20) {
+    tile_ilv<Cc, 1, true>(&mp.a, (int)row0, &mp.a, (int)col0, &mp.p, p, n_f, acc, smem);
+  } else if constexpr (V == 18 || V == 19) {
     tile_w16<Cc, V == 19>(&mp.a, (int)row0, &mp.a, (int)col0, &mp.p, p, n_f, acc, smem);
     store_tile_w16<Cc>(acc, out, n, row0, col0);
     return;
@@ -568,14 +577,14 @@ int main(int argc, char** argv) {
                               "own_a1_s6", "own_a2_s6", "prod_s6", "tma2_s6", "gen_d3_s6",
                               "gen_box_noxf_s6", "gen_nofence_s6", "gen_nobox_s6",
                               "gen_d4_s6", "ilv_a1_s4", "ilv_a1_s5", "ilv_a1_s6",
-                              "ilv_a2_s6", "w16_tma2_s4", "w16_ilv_a1_s4"};
+                              "ilv_a2_s6", "w16_tma2_s4", "w16_ilv_a1_s4", "ilv_pair_s4"};
   const void* fns[kVars] = {(const void*)k_var<0>, (const void*)k_var<1>, (const void*)k_var<2>,
                             (const void*)k_var<3>, (const void*)k_var<4>, (const void*)k_var<5>,
                             (const void*)k_var<6>, (const void*)k_var<7>, (const void*)k_var<8>,
                             (const void*)k_var<9>, (const void*)k_var<10>, (const void*)k_var<11>,
                             (const void*)k_var<12>, (const void*)k_var<13>, (const void*)k_var<14>,
                             (const void*)k_var<15>, (const void*)k_var<16>, (const void*)k_var<17>,
-                            (const void*)k_var<18>, (const void*)k_var<19>};
+                            (const void*)k_var<18>, (const void*)k_var<19>, (const void*)k_var<20>};
   for (int v = 0; v < kVars; ++v) {
     const int sm = kStagesOf[v] * C::STAGE_ELEMS * (int)sizeof(double);
     cudaFuncSetAttribute(fns[v], cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
@@ -602,7 +611,8 @@ int main(int argc, char** argv) {
       case 16: k_var<16><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
       case 17: k_var<17><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
       case 18: k_var<18><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
-      default: k_var<19><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
+      case 19: k_var<19><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
+      default: k_var<20><<<(unsigned)tiles, kNT, sm>>>(mp, n, n_f, o); break;
     }
   };
   if (mask & 2) run(1, o1);

@@ -427,7 +427,13 @@ cfg4n24)
   timeout 1500 python bench.py --gpus 4 --config cfg4 --steps 2 --warmup 3 --no-cpu > $O/bench_cfg4_n4.json 2> $O/bench_cfg4_n4.err
   timeout 1500 python bench.py --gpus 2 --config cfg4 --steps 2 --warmup 3 --no-cpu > $O/bench_cfg4_n2.json 2> $O/bench_cfg4_n2.err
   ;;
+nn)
+  # 3-way harness: per-warp rewrite split between the warps of a pair (named barrier) vs ilv
+  O=gpurun_out/r02nn; mkdir -p $O
+  timeout 300 build/exp_pivot_tma 8192 10000 1064963 > $O/exp_pivot_tma_8192.jsonl 2>&1
+  timeout 300 build/exp_pivot_tma 4096 20000 1064963 > $O/exp_pivot_tma_4096.jsonl 2>&1
+  ;;
 *)
-  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh final4 ii jj kk final1 final2 ll mm scale4 cfg5n4 par4 f32ncu final1b cfg4n24>"; exit 2
+  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh final4 ii jj kk final1 final2 ll mm scale4 cfg5n4 par4 f32ncu final1b cfg4n24 nn>"; exit 2
   ;;
 esac
