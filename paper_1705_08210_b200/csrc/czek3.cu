@@ -98,26 +98,36 @@ __device__ __forceinline__ void czek3_epilogue_single(const Czek3Box& b, const T
     for (int mi = 0; mi < TM; ++mi)
       nik[mi] = (okc && ty + 16 * mi < d.nr0) ? __ldg(nac + (ty + 16 * mi) + lk * b.ldAC) : T(0);
   };
+  // PSIM_EPI_COLS columns' loads in flight at a time (A/B define; 1 = product)
+#ifndef PSIM_EPI_COLS
+#define PSIM_EPI_COLS 1
+#endif
+  constexpr int G = PSIM_EPI_COLS;
 #pragma unroll
-  for (int nk = 0; nk < TN; ++nk) {
-    const int lk = tx + 16 * nk;
-    if (lk >= d.nc0) continue;
-    T nik[TM], njk, sk;
-    load_col(nk, nik, njk, sk);
-    const uint64_t kj = (uint64_t)(d.col0 + lk - j - 1);
+  for (int nk0 = 0; nk0 < TN; nk0 += G) {
+    T nik[G][TM], njk[G], sk[G];
 #pragma unroll
-    for (int mi = 0; mi < TM; ++mi) {
-      const int li = ty + 16 * mi;
-      if (li >= d.nr0) continue;
-      // metrics3.py:38-44, canonical roles: 1.5 (((n_ij + n_ik) + n_jk) - n_ijk) / ((s_i + s_j) + s_k)
-      const T n3 = Traits<T>::sub(Traits<T>::add(Traits<T>::add(nij[mi], nik[mi]), njk),
-                                  acc[mi][nk]);
-      const T dd = Traits<T>::add(sij[mi], sk);
-      const bool zero = dd == T(0);
-      const T v = zero ? T(0) : Traits<T>::div(Traits<T>::mul(T(1.5), n3), dd);
-      if (out) out[obase + li * ncols + lk] = v;
-      c.term(bij[mi] + kj, Traits<T>::bits(v));
-      c.deg += zero ? 1ull : 0ull;
+    for (int g = 0; g < G; ++g) load_col(nk0 + g, nik[g], njk[g], sk[g]);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int nk = nk0 + g;
+      const int lk = tx + 16 * nk;
+      if (lk >= d.nc0) continue;
+      const uint64_t kj = (uint64_t)(d.col0 + lk - j - 1);
+#pragma unroll
+      for (int mi = 0; mi < TM; ++mi) {
+        const int li = ty + 16 * mi;
+        if (li >= d.nr0) continue;
+        // metrics3.py:38-44, canonical roles: 1.5 (((n_ij + n_ik) + n_jk) - n_ijk) / ((s_i + s_j) + s_k)
+        const T n3 = Traits<T>::sub(Traits<T>::add(Traits<T>::add(nij[mi], nik[g][mi]), njk[g]),
+                                    acc[mi][nk]);
+        const T dd = Traits<T>::add(sij[mi], sk[g]);
+        const bool zero = dd == T(0);
+        const T v = zero ? T(0) : Traits<T>::div(Traits<T>::mul(T(1.5), n3), dd);
+        if (out) out[obase + li * ncols + lk] = v;
+        c.term(bij[mi] + kj, Traits<T>::bits(v));
+        c.deg += zero ? 1ull : 0ull;
+      }
     }
   }
 }

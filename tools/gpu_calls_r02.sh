@@ -433,7 +433,16 @@ nn)
   timeout 300 build/exp_pivot_tma 8192 10000 1064963 > $O/exp_pivot_tma_8192.jsonl 2>&1
   timeout 300 build/exp_pivot_tma 4096 20000 1064963 > $O/exp_pivot_tma_4096.jsonl 2>&1
   ;;
+oo)
+  # 3-way single-pivot epilogue: one column's loads in flight (product) vs two (build/ab/epi2)
+  O=gpurun_out/r02oo; mkdir -p $O
+  for r in 1 2; do
+    timeout 300 python tools/exp_box3.py 10000 "volume 1024" >> $O/prod.jsonl 2>> $O/prod.err
+    PSIM_LIB=build/ab/epi2/libpsim.so timeout 300 python tools/exp_box3.py 10000 "volume 1024" >> $O/epi2.jsonl 2>> $O/epi2.err
+  done
+  timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "3way or czek3 or box or config_shaped or golden" > $O/pytest_3.log 2>&1; echo "rc=$?" >> $O/pytest_3.log
+  ;;
 *)
-  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh final4 ii jj kk final1 final2 ll mm scale4 cfg5n4 par4 f32ncu final1b cfg4n24 nn>"; exit 2
+  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh final4 ii jj kk final1 final2 ll mm scale4 cfg5n4 par4 f32ncu final1b cfg4n24 nn oo>"; exit 2
   ;;
 esac
