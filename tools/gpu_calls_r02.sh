@@ -442,7 +442,15 @@ oo)
   done
   timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "3way or czek3 or box or config_shaped or golden" > $O/pytest_3.log 2>&1; echo "rc=$?" >> $O/pytest_3.log
   ;;
+final1c)
+  # last check of the round-end tree: GPU suite, smoke, cfg4 and cfg2 bench lines
+  O=gpurun_out/r02final1c; mkdir -p $O
+  timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "rc=$?" >> $O/smoke.log
+  timeout 900 python bench.py --config cfg4 --steps 2 --warmup 3 --no-cpu > $O/bench_cfg4.json 2> $O/bench_cfg4.err
+  timeout 900 python bench.py > $O/bench_cfg2.json 2> $O/bench_cfg2.err
+  ;;
 *)
-  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh final4 ii jj kk final1 final2 ll mm scale4 cfg5n4 par4 f32ncu final1b cfg4n24 nn oo>"; exit 2
+  echo "usage: $0 <call: a b c d e f g h i j k l m n o p q r s t u v w x y z aa bb cc z2 dd ee ff gg hh final4 ii jj kk final1 final2 ll mm scale4 cfg5n4 par4 f32ncu final1b cfg4n24 nn oo final1c>"; exit 2
   ;;
 esac
